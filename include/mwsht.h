@@ -1,0 +1,154 @@
+/*
+ * mwsht.h — C ABI of the B200-native McEwen–Wiaux spin spherical-harmonic
+ * transforms (libmwsht.so, built from paper_1110_6298_b200/csrc/).
+ *
+ * Drop-in boundary.  The reference (torusht, pure Python/numba) has no native
+ * ABI; its plugin/operator interface for this path is the Python entry points
+ * in pkg/src/torusht/mw.py and the kernel dispatchers in
+ * pkg/src/torusht/kernels/__init__.py.  Each entry point below replaces one of
+ * those (cited per function).  A host binding (paper_1110_6298_b200/_lib.py,
+ * ctypes) mirrors the reference's Python names, argument meaning and
+ * exception types on top of these calls; INTEGRATION.md shows the binding a
+ * maintainer of the reference would add.
+ *
+ * Conventions (identical to the reference):
+ *   - N = 2L-1.  Complex values are interleaved (re, im) float64 pairs
+ *     (numpy complex128 / C double _Complex layout).
+ *   - Flat coefficients: length L*L, index l(l+1)+m, 0 <= l < L, |m| <= l.
+ *   - Samples: (L, N) row-major, theta_t = pi(2t+1)/N rows, phi_p = 2 pi p/N cols.
+ *   - 2-D coefficient tables (kernel hooks): (L, N), column L-1+m.
+ *   - gfold (kernel hooks): (N, L), row L-1+m, column m' >= 0.
+ *   - All data pointers are DEVICE pointers on the plan's device unless the
+ *     name says _host.  Inputs are read-only; outputs are fully overwritten.
+ *   - `stream` is a cudaStream_t (0 = legacy default stream).  Calls are
+ *     asynchronous with respect to the host except where noted; one plan may
+ *     be used from one stream at a time (plans own scratch buffers).
+ *   - `recursion`: MWSHT_TRAPANI or MWSHT_RISBO.  Both are accepted for
+ *     drop-in compatibility (mw.py:43,562-566); both run the same stable GPU
+ *     recursions (inverse: l-recursion, forward: exponent-scaled Trapani
+ *     columns), so neither reproduces the reference Trapani's l>~1040
+ *     divergence.
+ *
+ * Every function returns an mwsht_status; the host binding maps it 1:1 onto
+ * the reference's exception types (errors.py:8-33).
+ */
+#ifndef MWSHT_H
+#define MWSHT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MWSHT_OK = 0,
+  MWSHT_E_BAND_LIMIT = 1,   /* InvalidBandLimitError   (grid.py:37-42)            */
+  MWSHT_E_SPIN = 2,         /* InvalidSpinError        (mw.py:121-126, 476-479)   */
+  MWSHT_E_CONTRACT = 3,     /* ContractViolationError  (mw.py:61-71, 94-98, 429)  */
+  MWSHT_E_SYMMETRY = 4,     /* SymmetryError           (mw.py:543-547)            */
+  MWSHT_E_VALUE = 5,        /* ValueError: unknown recursion (mw.py:562-566)      */
+  MWSHT_E_CUDA = 6,         /* CUDA runtime failure                              */
+  MWSHT_E_CUFFT = 7,        /* cuFFT failure                                     */
+  MWSHT_E_NOMEM = 8,        /* device or host allocation failure                 */
+  MWSHT_E_PLAN = 9          /* null / mismatched plan                            */
+} mwsht_status;
+
+typedef enum { MWSHT_TRAPANI = 0, MWSHT_RISBO = 1 } mwsht_recursion;
+
+typedef struct mwsht_plan mwsht_plan;
+
+/* Library / device introspection. */
+const char *mwsht_version(void);
+const char *mwsht_status_string(int status);
+/* Last CUDA / cuFFT error text recorded by this thread (for diagnostics). */
+const char *mwsht_last_error(void);
+
+/* Plan for band-limit L on `device` (cudaGetDevice() if < 0).  Owns the cuFFT
+ * plans, the quadrature-weight spectrum (cf. the reference's _CONV_CACHE,
+ * mw.py:225-241), the 1-D recursion tables, the l-independent top-row seed
+ * table sqrt(C(2n,n+k))/2^n, per-spin spin-column tables (built lazily), and
+ * scratch buffers for up to `max_batch` maps.  Creation synchronises. */
+int mwsht_plan_create(int L, int device, int max_batch, mwsht_plan **out);
+int mwsht_plan_destroy(mwsht_plan *plan);
+/* Device bytes currently held by the plan (tables + scratch). */
+size_t mwsht_plan_device_bytes(const mwsht_plan *plan);
+/* Build the spin-s tables now (otherwise built on first use; synchronises). */
+int mwsht_plan_prepare_spin(mwsht_plan *plan, int spin);
+
+/* ---------------------------------------------------------------- transforms */
+
+/* forward(signal, recursion) -> HarmonicCoeffs          (mw.py:365-375)
+ * samples: (L, N) complex;  flm: (L*L,) complex. */
+int mwsht_forward_z(mwsht_plan *plan, const void *samples, void *flm, int spin,
+                    int recursion, void *stream);
+
+/* inverse(coeffs, recursion) -> MwSignal                (mw.py:419-438)
+ * flm: (L*L,) complex (entries l < |spin| must be zero: checked by the host
+ * binding, mw.py:429-434);  samples: (L, N) complex. */
+int mwsht_inverse_z(mwsht_plan *plan, const void *flm, void *samples, int spin,
+                    int recursion, void *stream);
+
+/* forward_real(signal, recursion), spin 0                (mw.py:469-501)
+ * samples: (L, N) float64;  flm: (L*L,) complex (m < 0 rebuilt from the
+ * reality condition, mw.py:514-521). */
+int mwsht_forward_real_d(mwsht_plan *plan, const double *samples, void *flm, int recursion,
+                         void *stream);
+
+/* inverse_real(coeffs, recursion), spin 0                (mw.py:524-559)
+ * flm: (L*L,) complex satisfying conj(f_lm) = (-1)^m f_l,-m (checked by
+ * mwsht_reality_residual);  samples: (L, N) float64. */
+int mwsht_inverse_real_d(mwsht_plan *plan, const void *flm, double *samples, int recursion,
+                         void *stream);
+
+/* Reality check of inverse_real (mw.py:537-547): writes the worst residual
+ * max|conj(f) - (-1)^m f_{l,-m}| and the tolerance 1e-12*max(1, max|f|) to
+ * host memory.  Synchronises `stream`. */
+int mwsht_reality_residual(mwsht_plan *plan, const void *flm, double *worst_host,
+                           double *tol_host, void *stream);
+
+/* Batched transforms over `nmaps` independent maps laid out back to back
+ * (map stride L*L for coefficients, L*N for samples); nmaps <= max_batch.
+ * Same per-map semantics as the single-map calls (the callers'
+ * cli.py:159-224 loop over maps). */
+int mwsht_forward_z_batch(mwsht_plan *plan, int nmaps, const void *samples, void *flm,
+                          int spin, int recursion, void *stream);
+int mwsht_inverse_z_batch(mwsht_plan *plan, int nmaps, const void *flm, void *samples,
+                          int spin, int recursion, void *stream);
+
+/* --------------------------------------------------- kernel-level hooks ----
+ * Mirrors of torusht.kernels dispatchers (kernels/__init__.py:67-80) on
+ * device buffers, for stage-by-stage parity (test_kernels.py:52-92). */
+
+/* fmm_core(flm2d, cl, L, spin, use_trapani) -> T         (_numba.py:74-105)
+ * flm2d: (L, N) complex; cl: (L,) float64; T: (L, N) complex. */
+int mwsht_fmm_core(mwsht_plan *plan, const void *flm2d, const double *cl, int spin,
+                   int use_trapani, void *T, void *stream);
+/* flm_core(gfold, L, spin, use_trapani) -> R             (_numba.py:131-166)
+ * gfold: (N, L) complex; R: (L, N) complex. */
+int mwsht_flm_core(mwsht_plan *plan, const void *gfold, int spin, int use_trapani, void *R,
+                   void *stream);
+/* fmm_core_real(flm_half, cl, L, use_trapani) -> T       (_numba.py:108-128)
+ * flm_half, T: (L, L) complex. */
+int mwsht_fmm_core_real(mwsht_plan *plan, const void *flm_half, const double *cl,
+                        int use_trapani, void *T, void *stream);
+/* flm_core_real(gfold, L, use_trapani) -> R              (_numba.py:169-188)
+ * gfold, R: (L, L) complex. */
+int mwsht_flm_core_real(mwsht_plan *plan, const void *gfold, int use_trapani, void *R,
+                        void *stream);
+
+/* Forward FFT stages only: samples (L, N) complex -> gfold (N, L) complex
+ * (phi_fft, periodic_extend, theta_fft, weighted_convolution, _fold_mprime:
+ * mw.py:149-285), for stage-level parity. */
+int mwsht_forward_stages_z(mwsht_plan *plan, const void *samples, void *gfold, int spin,
+                           void *stream);
+
+/* Kernel launches issued by the most recent transform call on this plan
+ * (own kernels only, cuFFT excluded / included). */
+int mwsht_plan_last_launches(const mwsht_plan *plan, int *own, int *cufft);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MWSHT_H */

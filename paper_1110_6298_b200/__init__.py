@@ -1,0 +1,22 @@
+"""B200-native McEwen-Wiaux spin spherical-harmonic transforms.
+
+Drop-in for the reference package's transform path (torusht: forward,
+inverse, forward_real, inverse_real, HarmonicCoeffs, MwSignal, the error
+types), computed by hand-written sm_100a FP64 kernels + cuFFT behind the C ABI
+in include/mwsht.h.  See DESIGN.md.
+"""
+
+from .errors import (ContractViolationError, ConvergenceError, DeviceError,
+                     InvalidBandLimitError, InvalidSpinError, SymmetryError, TorushtError,
+                     UnsupportedDegreeError)
+from .mw import (HarmonicCoeffs, MwSignal, Plan, check_band_limit, clear_plans, forward,
+                 forward_batch, forward_real, get_plan, inverse, inverse_batch, inverse_real,
+                 mw_grid_phis, mw_grid_thetas, reality_residual)
+
+__all__ = [
+    "HarmonicCoeffs", "MwSignal", "forward", "inverse", "forward_real", "inverse_real",
+    "forward_batch", "inverse_batch", "reality_residual", "check_band_limit",
+    "mw_grid_thetas", "mw_grid_phis", "Plan", "get_plan", "clear_plans",
+    "TorushtError", "InvalidBandLimitError", "InvalidSpinError", "ContractViolationError",
+    "UnsupportedDegreeError", "SymmetryError", "ConvergenceError", "DeviceError",
+]

@@ -1,0 +1,118 @@
+// Shared definitions for the sm_100a MW transform kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mwsht {
+
+// ---------------------------------------------------------------------------
+// Recursion tables (device pointers), built once per band-limit on the host in
+// 80-bit long double and rounded once to float64 (plan.cu).  With
+//   A(0)=A(1)=1, A(k+2)=A(k) sqrt((k+1)/(k+2))
+//   V(k)=A(k)/(sqrt(k+1) A(k+1))
+//   Bt(Q)=Bt(Q-1)=1 (Q=2L+1), Bt(q)=Bt(q+2) sqrt((q+2)/(q+1))
+//   alpha(p)=2A(p-1)/(A(p) sqrt p), beta(q)=Bt(q+1)/(Bt(q) sqrt(q+1))
+//   lam(0)=lam(1)=1, lam(l+1)=lam(l-1)(l+1)/l, kap(l)=(2l+1)lam(l)/(l lam(l+1))
+// the two recursions in DESIGN.md §3 are
+//   inverse (l-recursion, chain (m',m)):
+//     Delta^l_{m'm} = (-1)^l lam_l u_l(m) u_l(m') z^l,  u_l(x)=A(l-x)A(l+x)
+//     z^{l+1} = kap_l C_l(m) C_l(m') z^l - z^{l-1},      C_l(x)=x V(l-x) V(l+x)
+//   forward (Trapani column, chain (l,m), walking mu=m' downward):
+//     Delta^l_{mu,m} = A(l-mu) Bt(l+mu) y_mu
+//     y_{mu-1} = m alpha(l-mu+1) beta(l+mu-1) y_mu - y_{mu+1}
+// ---------------------------------------------------------------------------
+struct DevTables {
+  int L, N;
+  const double* A;      // [2L+4]
+  const double* V;      // [2L+4]
+  const double* Bt;     // [2L+4]
+  const double* alpha;  // [2L+4]
+  const double* beta;   // [2L+4]
+  const double* lam;    // [L+2]
+  const double* kap;    // [L+2]
+  const double* cl;     // [L]   sqrt((2l+1)/4pi), as numpy computes it (mw.py:144-146)
+  const double* seed_mant;  // triangle n(n+1)/2+k : mantissa of sqrt(C(2n,n+k))/2^n
+  const int* seed_exp;      //                      : binary exponent
+};
+
+// Exponent-level machinery.  A chain whose true value is
+// below 2^-568 carries a level lev>0 with stored value z = true * 2^(768 lev),
+// |z| <= 2^200.  It contributes nothing while lev>0 (|true| < 2^-568) and is
+// rescaled by 2^-768 when |z| reaches 2^200.
+constexpr int kLevShift = 768;
+constexpr int kLevTop = 200;
+
+__device__ __forceinline__ double pow2i(int e) {
+  // 2^e for -1022 <= e <= 1023
+  return __hiloint2double((e + 1023) << 20, 0);
+}
+
+// true value = m * 2^ex (m a double of modest magnitude): returns stored z, lev.
+__device__ __forceinline__ double split_level(double m, int ex, int& lev) {
+  if (m == 0.0) {
+    lev = 0;
+    return 0.0;
+  }
+  int e2;
+  double f = frexp(m, &e2);  // m = f * 2^e2, 0.5 <= |f| < 1
+  int X = ex + e2;
+  int l = (kLevTop - X) / kLevShift;  // X <= 200 always here (values <= ~1)
+  if (X > kLevTop) l = 0;
+  if (l < 0) l = 0;
+  lev = l;
+  return ldexp(f, X + kLevShift * l);
+}
+
+// |z| >= 2^200 test on the high word (integer pipe, keeps the FP64 pipe free).
+__device__ __forceinline__ bool above_top(double z) {
+  return (__double2hiint(z) & 0x7ff00000) >= ((1023 + kLevTop) << 20);
+}
+
+__device__ __forceinline__ double seed_value(const DevTables& t, int n, int k, int& ex) {
+  long long idx = (long long)n * (n + 1) / 2 + k;
+  ex = t.seed_exp[idx];
+  return t.seed_mant[idx];
+}
+
+// i^p for p mod 4, as (re, im)
+__device__ __forceinline__ double2 ipow(int p) {
+  p &= 3;
+  return p == 0 ? make_double2(1, 0) : p == 1 ? make_double2(0, 1) : p == 2 ? make_double2(-1, 0)
+                                                                            : make_double2(0, -1);
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+
+// ---------------------------------------------------------------- core args
+constexpr int kThreads = 256;
+constexpr int kTileRows = 64;  // inverse: m' rows; forward: l rows
+constexpr int kTileCols = 32;  // m columns
+constexpr int kChunk = 16;     // l (inverse) or mu (forward) steps staged per smem fill
+
+struct InvArgs {
+  DevTables t;
+  const double* DW;     // [l*L + m'] = (-1)^l lam_l u_l(m') Delta^l_{m',-s}  (0 if m' > l or l < |s|)
+  const double* cl;     // per-degree weights (plan's or caller's)
+  const double2* in;    // flat flm (in_mode 0) or (L,N) table (in_mode 1) ; real: flat / (L,L)
+  double2* out;         // out_mode 0: theta-synthesis spectrum (N,N) [complex] / (L,N) [real]
+                        // out_mode 1: raw T (L,N) [complex] / (L,L) [real]
+  const int2* tiles;
+  int in_mode, out_mode, spin;
+  long long in_stride, out_stride;  // per-map element strides (batch = gridDim.y)
+};
+
+struct FwdArgs {
+  DevTables t;
+  const double* DW;     // [mu*L + l] = A(l-mu) Bt(l+mu) Delta^l_{mu,-s}  (0 if mu > l or l < |s|)
+  const double2* gf;    // complex: (N,L) rows L-1+m ; real: (L,L) rows m
+  double2* out;         // out_mode 0: flat flm (phases, c_l applied) ; 1: raw R (L,N) / (L,L)
+  const int2* tiles;
+  int out_mode, spin;
+  long long in_stride, out_stride;
+};
+
+}  // namespace mwsht

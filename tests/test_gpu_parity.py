@@ -1,0 +1,221 @@
+"""CUDA path vs the reference's own outputs (golden vectors) and the oracle.
+
+Tolerances (north_star: "relative max error of the order of 1e-12 at
+L <= 1024"): rel = max|gpu - ref| / max|ref| <= 1e-12 for every L <= 1024
+case, 2e-12 for the L = 1100 Risbo pin (the reference Risbo's own row-norm
+error there is ~4e-13), and the reference tests' absolute bounds for the tiny
+cases (test_mw.py:44-53: 1e-12).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden_cfg
+from helpers import SMALL_CASES, checksums, max_abs, random_signal, rel
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def mw():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import paper_1110_6298_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import mw_oracle
+    return mw_oracle
+
+
+# ----------------------------------------------------------- kernel level
+
+@pytest.mark.parametrize("spin", [0, 2, -1])
+@pytest.mark.parametrize("rec", ["trapani", "risbo"])
+def test_kernel_cores_match_reference(mw, golden_small, spin, rec):
+    from paper_1110_6298_b200 import kernels
+    L = 9
+    key = f"k9_s{spin}_{rec}"
+    cl = np.sqrt((2.0 * np.arange(L) + 1.0) / (4.0 * math.pi))
+    T = kernels.fmm_core(golden_small[key + "_flm2d"], cl, L, spin, rec == "trapani")
+    R = kernels.flm_core(golden_small[key + "_gfold"], L, spin, rec == "trapani")
+    assert max_abs(T, golden_small[key + "_fmm"]) < 1e-14
+    assert max_abs(R, golden_small[key + "_flm"]) < 1e-14
+
+
+def test_real_kernel_cores_match_reference(mw, golden_small):
+    from paper_1110_6298_b200 import kernels
+    cl = np.sqrt((2.0 * np.arange(8) + 1.0) / (4.0 * math.pi))
+    T = kernels.fmm_core_real(golden_small["k8real_in"], cl, 8, True)
+    R = kernels.flm_core_real(golden_small["k8real_gf"], 8, True)
+    assert max_abs(T, golden_small["k8real_fmm"]) < 1e-14
+    assert max_abs(R, golden_small["k8real_flm"]) < 1e-14
+
+
+@pytest.mark.parametrize("L,spin", [(1, 0), (2, 1), (5, -2), (33, 0), (70, 3), (130, 0),
+                                    (200, -7)])
+def test_kernel_cores_match_oracle(mw, O, L, spin):
+    from paper_1110_6298_b200 import kernels
+    rng = np.random.default_rng(L * 31 + spin)
+    flm2d = rng.standard_normal((L, 2 * L - 1)) + 1j * rng.standard_normal((L, 2 * L - 1))
+    gfold = rng.standard_normal((2 * L - 1, L)) + 1j * rng.standard_normal((2 * L - 1, L))
+    cl = O.cl_table(L)
+    T = kernels.fmm_core(flm2d, cl, L, spin, True)
+    R = kernels.flm_core(gfold, L, spin, True)
+    assert rel(T, O.fmm_core(flm2d, cl, L, spin, True, threads=4)) < REL_TOL
+    assert rel(R, O.flm_core(gfold, L, spin, True, threads=4)) < REL_TOL
+    if spin == 0:
+        half = np.ascontiguousarray(flm2d[:, L - 1:])
+        gh = np.ascontiguousarray(gfold[:L])
+        assert rel(kernels.fmm_core_real(half, cl, L, True),
+                   O.fmm_core_real(half, cl, L, True)) < REL_TOL
+        assert rel(kernels.flm_core_real(gh, L, True), O.flm_core_real(gh, L, True)) < REL_TOL
+
+
+@pytest.mark.parametrize("L,spin", [(1, 0), (4, 3), (16, -2), (64, 0), (127, 5)])
+def test_forward_stages_match_oracle(mw, O, L, spin):
+    from paper_1110_6298_b200 import kernels
+    sig = random_signal(L, spin, 3)
+    assert rel(kernels.forward_stages(sig, L, spin), O.gfold_of(sig, L, spin)) < 1e-13
+
+
+# --------------------------------------------------------- transforms
+
+@pytest.mark.parametrize("rec", ["trapani", "risbo"])
+@pytest.mark.parametrize("L,spin", SMALL_CASES)
+def test_small_transforms_match_reference(mw, O, golden_small, L, spin, rec):
+    key = f"L{L}_s{spin}_{rec}"
+    v = O.gaussian_coeffs(L, spin, L + abs(spin))
+    sig = mw.inverse(mw.HarmonicCoeffs(L, spin, v.copy()), recursion=rec).samples
+    assert max_abs(sig, golden_small[key + "_samples"]) < 1e-12
+    back = mw.forward(mw.MwSignal(L, spin, np.array(sig)), recursion=rec).values
+    assert max_abs(back, golden_small[key + "_back"]) < 1e-12
+    assert max_abs(back, v) < 1e-12   # round trip (test_mw.py:44-53)
+    raw = random_signal(L, spin, L + abs(spin))
+    fr = mw.forward(mw.MwSignal(L, spin, raw), recursion=rec).values
+    assert max_abs(fr, golden_small[key + "_fwdraw"]) < 1e-12
+
+
+def test_real_path_small_matches_reference(mw, O, golden_small):
+    v = O.gaussian_real_coeffs(16, 6)
+    sig = mw.inverse_real(mw.HarmonicCoeffs(16, 0, v.copy())).samples
+    assert sig.dtype == np.float64
+    assert max_abs(sig, golden_small["real16_samples"]) < 1e-13
+    back = mw.forward_real(mw.MwSignal(16, 0, np.array(sig))).values
+    assert max_abs(back, golden_small["real16_back"]) < 1e-12
+
+
+def _cfg_check(mw, O, name, tol=REL_TOL):
+    g = golden_cfg(name)
+    L, spin, real = int(g["L"]), int(g["spin"]), bool(g["real"])
+    seed = int(g["seed"])
+    v = O.gaussian_real_coeffs(L, seed) if real else O.gaussian_coeffs(L, spin, seed)
+    assert np.allclose(checksums(v), g["input_checksums"], rtol=1e-13, atol=0)
+    if real:
+        sig = mw.inverse_real(mw.HarmonicCoeffs(L, 0, v.copy())).samples
+        back = mw.forward_real(mw.MwSignal(L, 0, np.array(sig))).values
+    else:
+        sig = mw.inverse(mw.HarmonicCoeffs(L, spin, v.copy())).samples
+        back = mw.forward(mw.MwSignal(L, spin, np.array(sig))).values
+    s_ref = g["samples_sub"]
+    s_gpu = np.asarray(sig).reshape(-1)[g["samples_idx"]]
+    b_ref = g["back_sub"]
+    b_gpu = np.asarray(back)[g["back_idx"]]
+    r_s = max_abs(s_gpu, s_ref) / g["samples_checksums"][3]
+    r_b = max_abs(b_gpu, b_ref) / g["back_checksums"][3]
+    assert r_s < tol, r_s
+    assert r_b < tol, r_b
+    assert np.allclose(checksums(sig), g["samples_checksums"], rtol=1e-10, atol=1e-9)
+    assert np.allclose(checksums(back), g["back_checksums"], rtol=1e-10, atol=1e-9)
+    return r_s, r_b
+
+
+def test_config1_L64(mw, O):
+    _cfg_check(mw, O, "L64_s0_trapani")
+
+
+@pytest.mark.parametrize("spin", [2, -2])
+def test_config2_L256(mw, O, spin):
+    _cfg_check(mw, O, f"L256_s{spin}_trapani")
+
+
+def test_config3_L1024_real(mw, O):
+    _cfg_check(mw, O, "L1024_s0_trapani_real")
+
+
+def test_L1100_risbo_past_trapani_breakdown(mw, O):
+    _cfg_check(mw, O, "L1100_s0_risbo", tol=2e-12)
+
+
+@pytest.mark.parametrize("L,spin", [(256, 2), (300, -3), (512, 0)])
+def test_full_arrays_match_oracle(mw, O, L, spin):
+    v = O.gaussian_coeffs(L, spin, 11)
+    sig = mw.inverse(mw.HarmonicCoeffs(L, spin, v.copy())).samples
+    ref_sig = O.inverse(v, L, spin, threads=8)
+    assert rel(sig, ref_sig) < REL_TOL
+    back = mw.forward(mw.MwSignal(L, spin, np.array(sig))).values
+    assert rel(back, O.forward(ref_sig, L, spin, threads=8)) < REL_TOL
+    assert max_abs(back, v) < 1e-11
+
+
+# ----------------------------------------------------- semantics / errors
+
+def test_errors_match_reference_types(mw, O):
+    L = 6
+    with pytest.raises(mw.InvalidSpinError):
+        mw.inverse(mw.HarmonicCoeffs(4, 4, np.zeros(16, complex)))
+    with pytest.raises(mw.SymmetryError):
+        mw.inverse_real(mw.HarmonicCoeffs(5, 0, O.gaussian_coeffs(5, 0, 1)))
+    with pytest.raises(mw.InvalidSpinError):
+        mw.inverse_real(mw.HarmonicCoeffs(6, 1, O.gaussian_coeffs(6, 1, 0)))
+    sig = mw.inverse_real(mw.HarmonicCoeffs(L, 0, O.gaussian_real_coeffs(L, 7))).samples
+    with pytest.raises(mw.ContractViolationError):
+        mw.forward_real(mw.MwSignal(L, 0, sig + 1e-3j))
+    relaxed = mw.forward_real(mw.MwSignal(L, 0, sig.astype(np.complex128))).values
+    assert max_abs(relaxed, mw.forward_real(mw.MwSignal(L, 0, sig)).values) == 0.0
+    with pytest.raises(ValueError):
+        mw.forward(mw.MwSignal(3, 0, np.zeros((3, 5), complex)), recursion="fourier")
+
+
+def test_torch_tensors_stay_on_device(mw, O):
+    import torch
+    L, s = 40, 1
+    v = torch.from_numpy(O.gaussian_coeffs(L, s, 2)).cuda()
+    sig = mw.inverse(mw.HarmonicCoeffs(L, s, v)).samples
+    assert isinstance(sig, torch.Tensor) and sig.is_cuda
+    back = mw.forward(mw.MwSignal(L, s, sig)).values
+    assert isinstance(back, torch.Tensor) and back.is_cuda
+    assert (back - v).abs().max().item() < 1e-12
+
+
+def test_batched_matches_single(mw, O):
+    L, s, B = 48, 2, 3
+    vals = np.stack([O.gaussian_coeffs(L, s, k) for k in range(B)])
+    sig = mw.inverse_batch(vals, L, s)
+    for b in range(B):
+        one = mw.inverse(mw.HarmonicCoeffs(L, s, vals[b].copy())).samples
+        assert max_abs(sig[b], one) == 0.0
+    back = mw.forward_batch(sig, L, s)
+    for b in range(B):
+        one = mw.forward(mw.MwSignal(L, s, np.array(sig[b]))).values
+        assert max_abs(back[b], one) == 0.0
+        assert max_abs(back[b], vals[b]) < 1e-12
+
+
+def test_basis_vectors_round_trip(mw):
+    # test_mw.py:56-64
+    L = 8
+    for spin in (0, 1):
+        for ell in range(abs(spin), L):
+            for m in range(-ell, ell + 1):
+                values = np.zeros(L * L, dtype=np.complex128)
+                values[ell * (ell + 1) + m] = 1.0
+                out = mw.forward(mw.inverse(mw.HarmonicCoeffs(L, spin, values)))
+                assert max_abs(out.values, values) < 1e-12, (ell, m)
