@@ -148,6 +148,18 @@ int mwsht_forward_stages_z(mwsht_plan *plan, const void *samples, void *gfold, i
  * (own kernels only, cuFFT excluded / included). */
 int mwsht_plan_last_launches(const mwsht_plan *plan, int *own, int *cufft);
 
+/* Per-call event timing of the O(L^3) core kernel (bench / roofline).  When
+ * enabled, each transform records CUDA events on its stream around the FFT
+ * stages and around the core kernel; last_timing synchronises on them. */
+int mwsht_plan_set_timing(mwsht_plan *plan, int on);
+/* inverse = 0: last forward call (stages_ms = FFT stages before the core);
+ * inverse = 1: last inverse call (stages_ms = 0, the core runs first). */
+int mwsht_plan_last_timing(mwsht_plan *plan, int inverse, float *core_ms, float *stages_ms);
+
+/* DFMA throughput probe (FP64 roofline denominator): TFLOP/s reached by a
+ * dependency-free FMA kernel on every SM, best of 5 ~10 ms runs. */
+int mwsht_fp64_probe(int device, double *tflops, double *ms);
+
 #ifdef __cplusplus
 }
 #endif

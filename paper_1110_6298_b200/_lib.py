@@ -53,6 +53,11 @@ _SIGS = {
     "mwsht_flm_core_real": ([_P, _P, _I, _P, _P], _I),
     "mwsht_forward_stages_z": ([_P, _P, _P, _I, _P], _I),
     "mwsht_plan_last_launches": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
+    "mwsht_plan_set_timing": ([_P, _I], _I),
+    "mwsht_plan_last_timing": ([_P, _I, ctypes.POINTER(ctypes.c_float),
+                                ctypes.POINTER(ctypes.c_float)], _I),
+    "mwsht_fp64_probe": ([_I, ctypes.POINTER(ctypes.c_double),
+                          ctypes.POINTER(ctypes.c_double)], _I),
 }
 
 EXPORTED = tuple(_SIGS)

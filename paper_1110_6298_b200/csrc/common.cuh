@@ -95,24 +95,75 @@ constexpr int kChunk = 16;     // l (inverse) or mu (forward) steps staged per s
 
 struct InvArgs {
   DevTables t;
-  const double* DW;     // [l*L + m'] = (-1)^l lam_l u_l(m') Delta^l_{m',-s}  (0 if m' > l or l < |s|)
+  const double* DW;     // [l*ldw + m'] = (-1)^l lam_l u_l(m') Delta^l_{m',-s}  (0 if m' > l or l < |s|)
   const double* cl;     // per-degree weights (plan's or caller's)
   const double2* in;    // flat flm (in_mode 0) or (L,N) table (in_mode 1) ; real: flat / (L,L)
   double2* out;         // out_mode 0: theta-synthesis spectrum (N,N) [complex] / (L,N) [real]
                         // out_mode 1: raw T (L,N) [complex] / (L,L) [real]
   const int2* tiles;
   int in_mode, out_mode, spin;
+  int ldw;                          // leading dimension of DW (L rounded up to 64)
   long long in_stride, out_stride;  // per-map element strides (batch = gridDim.y)
 };
 
 struct FwdArgs {
   DevTables t;
-  const double* DW;     // [mu*L + l] = A(l-mu) Bt(l+mu) Delta^l_{mu,-s}  (0 if mu > l or l < |s|)
-  const double2* gf;    // complex: (N,L) rows L-1+m ; real: (L,L) rows m
+  const double* DW;     // [mu*ldw + l] = A(l-mu) Bt(l+mu) Delta^l_{mu,-s}  (0 if mu > l or l < |s|)
+  const double2* gf;    // transposed folded plane gfT[m'][row]: complex (L,N) row L-1+m; real (L,L)
   double2* out;         // out_mode 0: flat flm (phases, c_l applied) ; 1: raw R (L,N) / (L,L)
   const int2* tiles;
   int out_mode, spin;
+  int ldw;
   long long in_stride, out_stride;
 };
+
+}  // namespace mwsht
+
+// ------------------------------------------------------- async bulk copies
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier,
+// used to stage per-chunk row/column data without occupying registers.
+namespace mwsht {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// global -> shared bulk copy of `bytes` (multiple of 16, both addresses 16-B aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 
 }  // namespace mwsht

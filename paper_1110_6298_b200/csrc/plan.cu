@@ -25,6 +25,7 @@ void launch_pad_twist(const double2* B, double2* C, int rows, int L, int N, int 
 void launch_mul_spectrum(double2* C, const double2* W, int P, long long nrows, cudaStream_t st);
 void launch_fold(bool real, const double2* C, double2* gf, int L, int P, int spin, long long cs,
                  long long gs, int nm, cudaStream_t st);
+void launch_transpose(const double2* in, double2* out, int rows, int cols, cudaStream_t st);
 void launch_untranspose(bool real, const double2* S, double2* Out, int L, int N, long long ss,
                         long long os, int nm, cudaStream_t st);
 void launch_reality(const double2* f, int L, unsigned long long* worst, unsigned long long* peak,
@@ -72,6 +73,7 @@ struct SpinTab {
 
 struct mwsht_plan {
   int L = 0, N = 0, P = 0, device = 0, max_batch = 1;
+  int ldw = 0;  // DW tables' leading dimension: L rounded up to the 64-wide tile
   DevTables tabs{};
   std::vector<void*> allocs;
   size_t bytes = 0;
@@ -86,6 +88,8 @@ struct mwsht_plan {
   size_t fft_work_size = 0;
   unsigned long long* red = nullptr;  // 2 slots for the reality check
   int own_launches = 0, cufft_launches = 0;
+  bool timing = false;
+  cudaEvent_t ev[2][3] = {};  // [forward|inverse][start, core start, core end]
   std::vector<double> h_A, h_Bt, h_lam;  // host copies for spin tables
   std::mutex mu;
 };
@@ -226,7 +230,8 @@ static int build_spin(mwsht_plan* p, int spin) {
   if (p->spins.count(spin)) return MWSHT_OK;
   typedef long double ld;
   const int L = p->L, cs = spin < 0 ? -spin : spin;
-  std::vector<double> inv((size_t)L * L, 0.0), fwd((size_t)L * L, 0.0);
+  const int Lp = p->ldw;
+  std::vector<double> inv((size_t)L * Lp, 0.0), fwd((size_t)L * Lp, 0.0);
   std::vector<ld> sq(2 * L + 4);
   for (size_t i = 0; i < sq.size(); i++) sq[i] = sqrtl((ld)i);
   std::vector<ld> t0sq(L);
@@ -253,8 +258,8 @@ static int build_spin(mwsht_plan* p, int spin) {
         const ld u = (ld)hA[l - x] * (ld)hA[l + x];
         ld vi = (ld)hlam[l] * u * dv;
         if (l & 1) vi = -vi;
-        inv[(size_t)l * L + x] = (double)vi;
-        fwd[(size_t)x * L + l] = (double)((ld)hA[l - x] * (ld)hBt[l + x] * dv);
+        inv[(size_t)l * Lp + x] = (double)vi;
+        fwd[(size_t)x * Lp + l] = (double)((ld)hA[l - x] * (ld)hBt[l + x] * dv);
       }
     }
   });
@@ -413,6 +418,7 @@ static InvArgs inv_args(mwsht_plan* p, int spin) {
   a.cl = p->tabs.cl;
   a.tiles = p->tiles_inv;
   a.spin = spin;
+  a.ldw = p->ldw;
   return a;
 }
 
@@ -422,6 +428,7 @@ static FwdArgs fwd_args(mwsht_plan* p, int spin) {
   a.DW = p->spins[spin].DWfwd;
   a.tiles = p->tiles_fwd;
   a.spin = spin;
+  a.ldw = p->ldw;
   return a;
 }
 
@@ -484,7 +491,9 @@ static int do_forward(mwsht_plan* p, int nm, const void* samples, void* flm, int
   cudaStream_t st = (cudaStream_t)stream;
   const int L = p->L;
   const long long gstride = real ? (long long)L * L : (long long)(2 * L - 1) * L;
+  if (p->timing) CU(cudaEventRecord(p->ev[0][0], st));
   if ((rc = forward_stages(p, nm, samples, real, spin, p->bufG, gstride, st))) return rc;
+  if (p->timing) CU(cudaEventRecord(p->ev[0][1], st));
   FwdArgs a = fwd_args(p, spin);
   a.gf = p->bufG;
   a.out = (double2*)flm;
@@ -493,6 +502,7 @@ static int do_forward(mwsht_plan* p, int nm, const void* samples, void* flm, int
   a.out_stride = (long long)L * L;
   launch_forward_core(a, p->ntiles_fwd, nm, real, st);
   LAUNCHED(p);
+  if (p->timing) CU(cudaEventRecord(p->ev[0][2], st));
   return MWSHT_OK;
 }
 
@@ -516,6 +526,10 @@ static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int
   FFT(cufftSetStream(hrow, st));
   FFT(cufftSetStream(hphi, st));
   // 1. core + phases + m' mirror + theta twist (mw.py:378-402, 445)
+  if (p->timing) {
+    CU(cudaEventRecord(p->ev[1][0], st));
+    CU(cudaEventRecord(p->ev[1][1], st));
+  }
   InvArgs a = inv_args(p, spin);
   a.in = (const double2*)flm;
   a.in_mode = 0;
@@ -525,6 +539,7 @@ static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int
   a.out_stride = (long long)rows * N;
   launch_inverse_core(a, p->ntiles_inv, nm, real, st);
   LAUNCHED(p);
+  if (p->timing) CU(cudaEventRecord(p->ev[1][2], st));
   // 2. theta synthesis (mw.py:446), unnormalised inverse FFT over m'
   FFT(cufftExecZ2Z(hrow, (cufftDoubleComplex*)p->bufB, (cufftDoubleComplex*)p->bufB, CUFFT_INVERSE));
   p->cufft_launches++;
@@ -583,6 +598,7 @@ int mwsht_plan_create(int L, int device, int max_batch, mwsht_plan** out) {
   p->L = L;
   p->N = 2 * L - 1;
   p->P = smooth_len(4 * L - 3);
+  p->ldw = (L + kTileRows - 1) / kTileRows * kTileRows;
   p->device = device;
   p->max_batch = max_batch;
   cudaError_t e = cudaSetDevice(device);
@@ -614,6 +630,9 @@ int mwsht_plan_destroy(mwsht_plan* p) {
   cudaSetDevice(p->device);
   cudaDeviceSynchronize();
   for (auto& kv : p->ffts) cufftDestroy(kv.second);
+  for (auto& d : p->ev)
+    for (auto& e : d)
+      if (e) cudaEventDestroy(e);
   for (void* q : p->allocs) cudaFree(q);
   delete p;
   return MWSHT_OK;
@@ -724,7 +743,9 @@ int mwsht_flm_core(mwsht_plan* p, const void* gfold, int spin, int use_trapani, 
   if ((rc = build_spin(p, spin))) return rc;
   p->own_launches = p->cufft_launches = 0;
   FwdArgs a = fwd_args(p, spin);
-  a.gf = (const double2*)gfold;
+  launch_transpose((const double2*)gfold, p->bufG, p->N, p->L, (cudaStream_t)stream);
+  LAUNCHED(p);
+  a.gf = p->bufG;
   a.out = (double2*)R;
   a.out_mode = 1;
   // entries |m| > l stay zero, as in the reference's np.zeros output
@@ -741,7 +762,9 @@ int mwsht_flm_core_real(mwsht_plan* p, const void* gfold, int use_trapani, void*
   std::lock_guard<std::mutex> lk(p->mu);
   p->own_launches = p->cufft_launches = 0;
   FwdArgs a = fwd_args(p, 0);
-  a.gf = (const double2*)gfold;
+  launch_transpose((const double2*)gfold, p->bufG, p->L, p->L, (cudaStream_t)stream);
+  LAUNCHED(p);
+  a.gf = p->bufG;
   a.out = (double2*)R;
   a.out_mode = 1;
   CU(cudaMemsetAsync(R, 0, sizeof(double2) * (size_t)p->L * p->L, (cudaStream_t)stream));
@@ -756,8 +779,36 @@ int mwsht_forward_stages_z(mwsht_plan* p, const void* samples, void* gfold, int 
   if ((rc = check_plan(p)) || (rc = check_spin(p, spin))) return rc;
   std::lock_guard<std::mutex> lk(p->mu);
   p->own_launches = p->cufft_launches = 0;
-  return forward_stages(p, 1, samples, false, spin, (double2*)gfold, (long long)p->N * p->L,
-                        (cudaStream_t)stream);
+  if ((rc = forward_stages(p, 1, samples, false, spin, p->bufG, (long long)p->N * p->L,
+                           (cudaStream_t)stream)))
+    return rc;
+  launch_transpose(p->bufG, (double2*)gfold, p->L, p->N, (cudaStream_t)stream);
+  LAUNCHED(p);
+  return MWSHT_OK;
+}
+
+int mwsht_plan_set_timing(mwsht_plan* p, int on) {
+  int rc;
+  if ((rc = check_plan(p))) return rc;
+  for (auto& d : p->ev)
+    for (auto& e : d)
+      if (!e) CU(cudaEventCreate(&e));
+  p->timing = on != 0;
+  return MWSHT_OK;
+}
+
+int mwsht_plan_last_timing(mwsht_plan* p, int inverse, float* core_ms, float* stages_ms) {
+  int rc;
+  if ((rc = check_plan(p))) return rc;
+  if (!p->timing) return fail(MWSHT_E_VALUE, "last_timing", "timing not enabled");
+  cudaEvent_t* e = p->ev[inverse ? 1 : 0];
+  CU(cudaEventSynchronize(e[2]));
+  float c = 0.f, s0 = 0.f;
+  CU(cudaEventElapsedTime(&c, e[1], e[2]));
+  CU(cudaEventElapsedTime(&s0, e[0], e[1]));
+  if (core_ms) *core_ms = c;
+  if (stages_ms) *stages_ms = s0;
+  return MWSHT_OK;
 }
 
 int mwsht_plan_last_launches(const mwsht_plan* p, int* own, int* cufft) {

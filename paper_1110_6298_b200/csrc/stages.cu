@@ -81,25 +81,56 @@ __global__ void k_mul_spectrum(double2* __restrict__ C, const double2* __restric
   }
 }
 
-// Forward: circular correlation output -> m'-folded plane (mw.py:251, 273-285, 504-511).
+// Forward: circular correlation output -> m'-folded plane (mw.py:251, 273-285, 504-511),
+// written transposed for the core's bulk copies: gfT[j][r] (rows = orders r).
 // G(m') = C[r][3L-3+m'];  gf[r][0] = G(0), gf[r][j] = G(j) + s_r G(-j),
 // s_r = (-1)^(m+s) (complex, m = r-(L-1)) or (-1)^r (real).
 template <bool REAL>
-__global__ void k_fold(const double2* __restrict__ C, double2* __restrict__ gf, int L, int P,
-                       int spin, long long c_stride, long long g_stride) {
-  const int r = blockIdx.y;
-  const double2* c = C + (long long)blockIdx.z * c_stride + (long long)r * P;
-  double2* g = gf + (long long)blockIdx.z * g_stride + (long long)r * L;
-  const int m = REAL ? r : r - (L - 1);
-  const double sr = ((m + (REAL ? 0 : spin)) & 1) ? -1.0 : 1.0;
+__global__ void k_fold_T(const double2* __restrict__ C, double2* __restrict__ gfT, int L, int P,
+                         int spin, long long c_stride, long long g_stride) {
+  __shared__ double2 tile[32][33];
+  const int rows = REAL ? L : 2 * L - 1;
+  const int jb = blockIdx.x * 32, rb = blockIdx.y * 32;
+  const double2* c = C + (long long)blockIdx.z * c_stride;
+  double2* g = gfT + (long long)blockIdx.z * g_stride;
+  const int tx = threadIdx.x, ty = threadIdx.y;
   const int o = 3 * L - 3;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L; j += gridDim.x * blockDim.x) {
-    double2 v = c[o + j];
-    if (j > 0) {
-      const double2 u = c[o - j];
-      v = make_double2(v.x + sr * u.x, v.y + sr * u.y);
+  for (int k = ty; k < 32; k += 8) {
+    const int r = rb + k, j = jb + tx;
+    double2 v = make_double2(0.0, 0.0);
+    if (r < rows && j < L) {
+      const double2* row = c + (long long)r * P;
+      v = row[o + j];
+      if (j > 0) {
+        const int m = REAL ? r : r - (L - 1);
+        const double sr = ((m + (REAL ? 0 : spin)) & 1) ? -1.0 : 1.0;
+        const double2 u = row[o - j];
+        v = make_double2(v.x + sr * u.x, v.y + sr * u.y);
+      }
     }
-    g[j] = v;
+    tile[k][tx] = v;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int j = jb + k, r = rb + tx;
+    if (j < L && r < rows) g[(long long)j * rows + r] = tile[tx][k];
+  }
+}
+
+// out[c][r] = in[r][c] for a (rows x cols) complex matrix.
+__global__ void k_transpose(const double2* __restrict__ in, double2* __restrict__ out, int rows,
+                            int cols) {
+  __shared__ double2 tile[32][33];
+  const int cb = blockIdx.x * 32, rb = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int k = ty; k < 32; k += 8) {
+    const int r = rb + k, c = cb + tx;
+    tile[k][tx] = (r < rows && c < cols) ? in[(long long)r * cols + c] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int c = cb + k, r = rb + tx;
+    if (c < cols && r < rows) out[(long long)c * rows + r] = tile[tx][k];
   }
 }
 
@@ -194,15 +225,19 @@ void launch_mul_spectrum(double2* C, const double2* W, int P, long long nrows, c
   k_mul_spectrum<<<(unsigned)blocks, 256, 0, st>>>(C, W, P, nrows);
 }
 
-void launch_fold(bool real, const double2* C, double2* gf, int L, int P, int spin, long long cs,
+void launch_fold(bool real, const double2* C, double2* gfT, int L, int P, int spin, long long cs,
                  long long gs, int nm, cudaStream_t st) {
   const int rows = real ? L : 2 * L - 1;
-  const int threads = 128;
-  dim3 grid((L + threads - 1) / threads, rows, nm);
+  dim3 grid((L + 31) / 32, (rows + 31) / 32, nm), block(32, 8);
   if (real)
-    k_fold<true><<<grid, threads, 0, st>>>(C, gf, L, P, spin, cs, gs);
+    k_fold_T<true><<<grid, block, 0, st>>>(C, gfT, L, P, spin, cs, gs);
   else
-    k_fold<false><<<grid, threads, 0, st>>>(C, gf, L, P, spin, cs, gs);
+    k_fold_T<false><<<grid, block, 0, st>>>(C, gfT, L, P, spin, cs, gs);
+}
+
+void launch_transpose(const double2* in, double2* out, int rows, int cols, cudaStream_t st) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32), block(32, 8);
+  k_transpose<<<grid, block, 0, st>>>(in, out, rows, cols);
 }
 
 void launch_untranspose(bool real, const double2* S, double2* Out, int L, int N, long long ss,
