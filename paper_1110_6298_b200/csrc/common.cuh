@@ -88,29 +88,35 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 
 // ---------------------------------------------------------------- core args
-constexpr int kThreads = 256;
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumerThreads = 32 * kConsumerWarps;
+constexpr int kCoreThreads = kConsumerThreads + 32;  // + one TMA producer warp
 constexpr int kTileRows = 64;  // inverse: m' rows; forward: l rows
 constexpr int kTileCols = 32;  // m columns
-constexpr int kChunk = 16;     // l (inverse) or mu (forward) steps staged per smem fill
+constexpr int kChunk = 16;     // l (inverse) or m' (forward) steps per pipeline stage
+constexpr int kStages = 4;     // depth of the mbarrier ring
 
+// All 2-D plan tables and staged planes have leading dimension ldw = L rounded
+// up to kTileRows, zero-padded, so every bulk copy is in bounds and aligned.
 struct InvArgs {
   DevTables t;
-  const double* DW;     // [l*ldw + m'] = (-1)^l lam_l u_l(m') Delta^l_{m',-s}  (0 if m' > l or l < |s|)
-  const double* cl;     // per-degree weights (plan's or caller's)
-  const double2* in;    // flat flm (in_mode 0) or (L,N) table (in_mode 1) ; real: flat / (L,L)
-  double2* out;         // out_mode 0: theta-synthesis spectrum (N,N) [complex] / (L,N) [real]
-                        // out_mode 1: raw T (L,N) [complex] / (L,L) [real]
+  const double2* rowtab;  // [l*ldw + m'] = (kap_l C_l(m'), (-1)^l lam_l u_l(m') Delta^l_{m',-s})
+  const double* colc;     // [l*ldw + m]  = C_l(m)
+  const double2* gp;      // pre-scaled coefficients: gp[l*ldw+m] = c_l u_l(m) f_{l,m},
+                          // gn = gp + L*ldw: c_l u_l(m) (-1)^l f_{l,-m}  (zero for m > l)
+  double2* out;           // out_mode 0: theta-synthesis spectrum (N,N) [complex] / (L,N) [real]
+                          // out_mode 1: raw T (L,N) [complex] / (L,L) [real]
   const int2* tiles;
-  int in_mode, out_mode, spin;
-  int ldw;                          // leading dimension of DW (L rounded up to 64)
-  long long in_stride, out_stride;  // per-map element strides (batch = gridDim.y)
+  int out_mode, spin;
+  int ldw;
+  long long g_stride, out_stride;  // per-map element strides (batch = gridDim.y)
 };
 
 struct FwdArgs {
   DevTables t;
-  const double* DW;     // [mu*ldw + l] = A(l-mu) Bt(l+mu) Delta^l_{mu,-s}  (0 if mu > l or l < |s|)
-  const double2* gf;    // transposed folded plane gfT[m'][row]: complex (L,N) row L-1+m; real (L,L)
-  double2* out;         // out_mode 0: flat flm (phases, c_l applied) ; 1: raw R (L,N) / (L,L)
+  const double2* rowtab;  // [m'*ldw + l] = (alpha(l-m'+1) beta(l+m'-1), A(l-m') Bt(l+m') Delta^l_{m',-s})
+  const double2* gf;      // gfT[m'*ldw + m] = gfold[+m][m'];  + L*ldw: (-1)^m' gfold[-m][m']
+  double2* out;           // out_mode 0: flat flm (phases, c_l applied) ; 1: raw R (L,N) / (L,L)
   const int2* tiles;
   int out_mode, spin;
   int ldw;
@@ -145,6 +151,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {

@@ -23,8 +23,12 @@ void launch_extend_transpose(bool real, const double2* A, double2* B, int L, int
 void launch_pad_twist(const double2* B, double2* C, int rows, int L, int N, int P, long long bs,
                       long long cs, int nm, cudaStream_t st);
 void launch_mul_spectrum(double2* C, const double2* W, int P, long long nrows, cudaStream_t st);
-void launch_fold(bool real, const double2* C, double2* gf, int L, int P, int spin, long long cs,
-                 long long gs, int nm, cudaStream_t st);
+void launch_fold(bool real, bool from_conv, const double2* src, double2* gfT, int L, int P,
+                 int ldw, int spin, long long ss, long long gs, int nm, cudaStream_t st);
+void launch_T2_to_fold(bool real, const double2* gfT, double2* gf, int L, int ldw, cudaStream_t st);
+void launch_inv_prescale(bool real, const double2* in, int in_mode, const double* cl,
+                         const double* A, int L, int ldw, double2* gp, long long is, long long gs,
+                         int nm, cudaStream_t st);
 void launch_transpose(const double2* in, double2* out, int rows, int cols, cudaStream_t st);
 void launch_untranspose(bool real, const double2* S, double2* Out, int L, int N, long long ss,
                         long long os, int nm, cudaStream_t st);
@@ -67,8 +71,8 @@ static int fail(int code, const char* what, const char* detail) {
 enum FftKind { F_PHI_Z = 0, F_PHI_D2Z, F_PHI_Z2D, F_ROWN, F_ROWP, F_ROWP_HALF, F_WSPEC };
 
 struct SpinTab {
-  double* DWinv = nullptr;
-  double* DWfwd = nullptr;
+  double2* rowinv = nullptr;  // [l*ldw + m'] = (kap_l C_l(m'), W_l(m'))
+  double2* rowfwd = nullptr;  // [m'*ldw + l] = (alpha(l-m'+1) beta(l+m'-1), W'(l, m'))
 };
 
 struct mwsht_plan {
@@ -90,7 +94,8 @@ struct mwsht_plan {
   int own_launches = 0, cufft_launches = 0;
   bool timing = false;
   cudaEvent_t ev[2][3] = {};  // [forward|inverse][start, core start, core end]
-  std::vector<double> h_A, h_Bt, h_lam;  // host copies for spin tables
+  double* colc = nullptr;  // [l*ldw + m] = C_l(m)
+  std::vector<long double> hl_A, hl_V, hl_Bt, hl_lam, hl_kap;  // host tables for the spin builds
   std::mutex mu;
 };
 
@@ -215,58 +220,78 @@ static int build_tables(mwsht_plan* p) {
   int* di;
   if ((rc = upload(p, &di, sexp))) return rc;
   T.seed_exp = di;
-  p->h_A = hA;
-  p->h_Bt = hBt;
-  p->h_lam = hlam;
+  p->hl_A = A;
+  p->hl_V = V;
+  p->hl_Bt = Bt;
+  p->hl_lam = lam;
+  p->hl_kap = kap;
+  // C_l(m) = m V(l-m) V(l+m) for m <= l (column factor of the l-recursion)
+  const int Lp = p->ldw;
+  std::vector<double> colc((size_t)L * Lp, 0.0);
+  host_parallel(L, [&](int lo, int hi) {
+    for (int l = lo; l < hi; l++)
+      for (int m = 0; m <= l; m++) colc[(size_t)l * Lp + m] = (double)((ld)m * V[l - m] * V[l + m]);
+  });
+  if ((rc = upload(p, &p->colc, colc))) return rc;
   return MWSHT_OK;
 }
 
-// Spin-column tables for spin s: Delta^l_{x,-s}, x <= l, from the Trapani
-// column recursion (_numba.py:63-71) run in 80-bit long double (its extended
-// exponent range removes the reference's float64 overflow), then
-//   DWinv[l*L + x] = (-1)^l lam_l u_l(x) Delta^l_{x,-s}
-//   DWfwd[x*L + l] = A(l-x) Bt(l+x) Delta^l_{x,-s}
+// Per-spin plan tables.  The spin column Delta^l_{x,-s}, x <= l, comes from
+// the Trapani column recursion (_numba.py:63-71) run in 80-bit long double
+// (whose exponent range removes the reference's float64 overflow), and is
+// packed with the recursion coefficients each core reads per step:
+//   rowinv[l*ldw + x] = (kap_l C_l(x),               (-1)^l lam_l u_l(x) Delta^l_{x,-s})
+//   rowfwd[x*ldw + l] = (alpha(l-x+1) beta(l+x-1),   A(l-x) Bt(l+x) Delta^l_{x,-s})
+// with C_l(x) = x V(l-x) V(l+x), u_l(x) = A(l-x) A(l+x)  (common.cuh).
 static int build_spin(mwsht_plan* p, int spin) {
   if (p->spins.count(spin)) return MWSHT_OK;
   typedef long double ld;
   const int L = p->L, cs = spin < 0 ? -spin : spin;
   const int Lp = p->ldw;
-  std::vector<double> inv((size_t)L * Lp, 0.0), fwd((size_t)L * Lp, 0.0);
+  std::vector<double2> inv((size_t)L * Lp, make_double2(0.0, 0.0)), fwd(inv);
   std::vector<ld> sq(2 * L + 4);
   for (size_t i = 0; i < sq.size(); i++) sq[i] = sqrtl((ld)i);
   std::vector<ld> t0sq(L);
   t0sq[0] = 1.0L;
   for (int j = 1; j < L; j++) t0sq[j] = t0sq[j - 1] * (ld)(2 * j - 1) / (ld)(2 * j);
-  const std::vector<double>&hA = p->h_A, &hBt = p->h_Bt, &hlam = p->h_lam;
+  const std::vector<ld>&A = p->hl_A, &V = p->hl_V, &Bt = p->hl_Bt, &lam = p->hl_lam,
+                      &kap = p->hl_kap;
   host_parallel(L, [&](int lo, int hi) {
     std::vector<ld> col(L + 2);
     for (int l = lo; l < hi; l++) {
-      if (l < cs) continue;
-      // seed Delta^l_{l,cs} = (-1)^(l-cs) sqrt(C(2l, l+cs))/2^l
-      ld P = t0sq[l];
-      for (int k = 0; k < cs; k++) P = P * (ld)(l - k) / (ld)(l + k + 1);
-      col[l + 1] = 0.0L;
-      col[l] = ((l - cs) & 1 ? -1.0L : 1.0L) * sqrtl(P);
-      for (int mu = l - 1; mu >= 0; mu--) {
-        const ld inv_ = 1.0L / (sq[l + mu + 1] * sq[l - mu]);
-        const ld c2 = (mu + 2 <= l) ? sq[l - mu - 1] * sq[l + mu + 2] : 0.0L;
-        col[mu] = (2.0L * cs * col[mu + 1] - c2 * col[mu + 2]) * inv_;
+      const bool has = l >= cs;
+      if (has) {
+        // seed Delta^l_{l,cs} = (-1)^(l-cs) sqrt(C(2l, l+cs))/2^l
+        ld P = t0sq[l];
+        for (int k = 0; k < cs; k++) P = P * (ld)(l - k) / (ld)(l + k + 1);
+        col[l + 1] = 0.0L;
+        col[l] = ((l - cs) & 1 ? -1.0L : 1.0L) * sqrtl(P);
+        for (int mu = l - 1; mu >= 0; mu--) {
+          const ld inv_ = 1.0L / (sq[l + mu + 1] * sq[l - mu]);
+          const ld c2 = (mu + 2 <= l) ? sq[l - mu - 1] * sq[l + mu + 2] : 0.0L;
+          col[mu] = (2.0L * cs * col[mu + 1] - c2 * col[mu + 2]) * inv_;
+        }
       }
       for (int x = 0; x <= l; x++) {
-        ld dv = col[x];
+        ld dv = has ? col[x] : 0.0L;
         if (spin > 0 && ((l + x) & 1)) dv = -dv;  // Delta_{x,-s} = (-1)^(l+x) Delta_{x,s}
-        const ld u = (ld)hA[l - x] * (ld)hA[l + x];
-        ld vi = (ld)hlam[l] * u * dv;
-        if (l & 1) vi = -vi;
-        inv[(size_t)l * Lp + x] = (double)vi;
-        fwd[(size_t)x * Lp + l] = (double)((ld)hA[l - x] * (ld)hBt[l + x] * dv);
+        ld wi = lam[l] * A[l - x] * A[l + x] * dv;
+        if (l & 1) wi = -wi;
+        const ld cx = kap[l] * (ld)x * V[l - x] * V[l + x];
+        inv[(size_t)l * Lp + x] = make_double2((double)cx, (double)wi);
+        ld qn = 0.0L;
+        if (x >= 1) {
+          const int pp = l - x + 1, qq = l + x - 1;
+          qn = (2.0L * A[pp - 1] / (A[pp] * sq[pp])) * (Bt[qq + 1] / (Bt[qq] * sq[qq + 1]));
+        }
+        fwd[(size_t)x * Lp + l] = make_double2((double)qn, (double)(A[l - x] * Bt[l + x] * dv));
       }
     }
   });
   SpinTab st;
   int rc;
-  if ((rc = upload(p, &st.DWinv, inv))) return rc;
-  if ((rc = upload(p, &st.DWfwd, fwd))) return rc;
+  if ((rc = upload(p, &st.rowinv, inv))) return rc;
+  if ((rc = upload(p, &st.rowfwd, fwd))) return rc;
   p->spins[spin] = st;
   return MWSHT_OK;
 }
@@ -414,8 +439,10 @@ static int check_spin(mwsht_plan* p, int spin) {
 static InvArgs inv_args(mwsht_plan* p, int spin) {
   InvArgs a{};
   a.t = p->tabs;
-  a.DW = p->spins[spin].DWinv;
-  a.cl = p->tabs.cl;
+  a.rowtab = p->spins[spin].rowinv;
+  a.colc = p->colc;
+  a.gp = p->bufG;
+  a.g_stride = p->strideG;
   a.tiles = p->tiles_inv;
   a.spin = spin;
   a.ldw = p->ldw;
@@ -425,16 +452,18 @@ static InvArgs inv_args(mwsht_plan* p, int spin) {
 static FwdArgs fwd_args(mwsht_plan* p, int spin) {
   FwdArgs a{};
   a.t = p->tabs;
-  a.DW = p->spins[spin].DWfwd;
+  a.rowtab = p->spins[spin].rowfwd;
+  a.gf = p->bufG;
+  a.in_stride = p->strideG;
   a.tiles = p->tiles_fwd;
   a.spin = spin;
   a.ldw = p->ldw;
   return a;
 }
 
-// samples (L,N) -> gfold (N,L) (complex) or real samples -> gfold (L,L)
+// samples (L,N) -> folded plane in the forward core's staging layout (bufG)
 static int forward_stages(mwsht_plan* p, int nm, const void* samples, bool real, int spin,
-                          double2* gf_out, long long gf_stride, cudaStream_t st) {
+                          cudaStream_t st) {
   const int L = p->L, N = p->N, P = p->P;
   cufftHandle hphi, hrow, hconv;
   int rc;
@@ -445,7 +474,7 @@ static int forward_stages(mwsht_plan* p, int nm, const void* samples, bool real,
   FFT(cufftSetStream(hrow, st));
   FFT(cufftSetStream(hconv, st));
   const int rows = real ? L : N;
-  // 1. phi FFT (mw.py:149-158 / :489); bufA stride: L*N complex per map
+  // 1. phi FFT (mw.py:149-158 / :489)
   if (real)
     FFT(cufftExecD2Z(hphi, (cufftDoubleReal*)samples, (cufftDoubleComplex*)p->bufA));
   else
@@ -471,8 +500,9 @@ static int forward_stages(mwsht_plan* p, int nm, const void* samples, bool real,
   LAUNCHED(p);
   FFT(cufftExecZ2Z(hconv, (cufftDoubleComplex*)p->bufC, (cufftDoubleComplex*)p->bufC, CUFFT_INVERSE));
   p->cufft_launches++;
-  // 6. extract + m' fold (mw.py:251, 273-285)
-  launch_fold(real, p->bufC, gf_out, L, P, spin, (long long)rows * P, gf_stride, nm, st);
+  // 6. extract + m' fold into the core's layout (mw.py:251, 273-285)
+  launch_fold(real, true, p->bufC, p->bufG, L, P, p->ldw, spin, (long long)rows * P, p->strideG,
+              nm, st);
   LAUNCHED(p);
   return MWSHT_OK;
 }
@@ -490,15 +520,12 @@ static int do_forward(mwsht_plan* p, int nm, const void* samples, void* flm, int
   p->own_launches = p->cufft_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
   const int L = p->L;
-  const long long gstride = real ? (long long)L * L : (long long)(2 * L - 1) * L;
   if (p->timing) CU(cudaEventRecord(p->ev[0][0], st));
-  if ((rc = forward_stages(p, nm, samples, real, spin, p->bufG, gstride, st))) return rc;
+  if ((rc = forward_stages(p, nm, samples, real, spin, st))) return rc;
   if (p->timing) CU(cudaEventRecord(p->ev[0][1], st));
   FwdArgs a = fwd_args(p, spin);
-  a.gf = p->bufG;
   a.out = (double2*)flm;
   a.out_mode = 0;
-  a.in_stride = gstride;
   a.out_stride = (long long)L * L;
   launch_forward_core(a, p->ntiles_fwd, nm, real, st);
   LAUNCHED(p);
@@ -525,17 +552,16 @@ static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int
   if ((rc = get_fft(p, real ? F_PHI_Z2D : F_PHI_Z, nm, &hphi))) return rc;
   FFT(cufftSetStream(hrow, st));
   FFT(cufftSetStream(hphi, st));
+  if (p->timing) CU(cudaEventRecord(p->ev[1][0], st));
+  // 0. unflatten + c_l u_l(m) scaling into the core's staging rows (mw.py:390-392)
+  launch_inv_prescale(real, (const double2*)flm, 0, p->tabs.cl, p->tabs.A, L, p->ldw, p->bufG,
+                      (long long)L * L, p->strideG, nm, st);
+  LAUNCHED(p);
   // 1. core + phases + m' mirror + theta twist (mw.py:378-402, 445)
-  if (p->timing) {
-    CU(cudaEventRecord(p->ev[1][0], st));
-    CU(cudaEventRecord(p->ev[1][1], st));
-  }
+  if (p->timing) CU(cudaEventRecord(p->ev[1][1], st));
   InvArgs a = inv_args(p, spin);
-  a.in = (const double2*)flm;
-  a.in_mode = 0;
   a.out = p->bufB;
   a.out_mode = 0;
-  a.in_stride = (long long)L * L;
   a.out_stride = (long long)rows * N;
   launch_inverse_core(a, p->ntiles_inv, nm, real, st);
   LAUNCHED(p);
@@ -610,7 +636,7 @@ int mwsht_plan_create(int L, int device, int max_batch, mwsht_plan** out) {
   p->strideA = L_ * N;
   p->strideB = N * N;
   p->strideC = N * P;
-  p->strideG = N * L_;
+  p->strideG = 2 * L_ * p->ldw;
   if ((rc = build_tables(p)) || (rc = build_tiles(p)) ||
       (rc = dev_alloc(p, (void**)&p->bufA, sizeof(double2) * p->strideA * max_batch)) ||
       (rc = dev_alloc(p, (void**)&p->bufB, sizeof(double2) * p->strideB * max_batch)) ||
@@ -705,13 +731,14 @@ int mwsht_fmm_core(mwsht_plan* p, const void* flm2d, const double* cl, int spin,
   std::lock_guard<std::mutex> lk(p->mu);
   if ((rc = build_spin(p, spin))) return rc;
   p->own_launches = p->cufft_launches = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  launch_inv_prescale(false, (const double2*)flm2d, 1, cl, p->tabs.A, p->L, p->ldw, p->bufG, 0,
+                      p->strideG, 1, st);
+  LAUNCHED(p);
   InvArgs a = inv_args(p, spin);
-  a.in = (const double2*)flm2d;
-  a.in_mode = 1;
-  a.cl = cl;
   a.out = (double2*)T;
   a.out_mode = 1;
-  launch_inverse_core(a, p->ntiles_inv, 1, false, (cudaStream_t)stream);
+  launch_inverse_core(a, p->ntiles_inv, 1, false, st);
   LAUNCHED(p);
   return MWSHT_OK;
 }
@@ -723,13 +750,14 @@ int mwsht_fmm_core_real(mwsht_plan* p, const void* flm_half, const double* cl, i
   (void)use_trapani;
   std::lock_guard<std::mutex> lk(p->mu);
   p->own_launches = p->cufft_launches = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  launch_inv_prescale(true, (const double2*)flm_half, 1, cl, p->tabs.A, p->L, p->ldw, p->bufG, 0,
+                      p->strideG, 1, st);
+  LAUNCHED(p);
   InvArgs a = inv_args(p, 0);
-  a.in = (const double2*)flm_half;
-  a.in_mode = 1;
-  a.cl = cl;
   a.out = (double2*)T;
   a.out_mode = 1;
-  launch_inverse_core(a, p->ntiles_inv, 1, true, (cudaStream_t)stream);
+  launch_inverse_core(a, p->ntiles_inv, 1, true, st);
   LAUNCHED(p);
   return MWSHT_OK;
 }
@@ -742,15 +770,16 @@ int mwsht_flm_core(mwsht_plan* p, const void* gfold, int spin, int use_trapani, 
   std::lock_guard<std::mutex> lk(p->mu);
   if ((rc = build_spin(p, spin))) return rc;
   p->own_launches = p->cufft_launches = 0;
-  FwdArgs a = fwd_args(p, spin);
-  launch_transpose((const double2*)gfold, p->bufG, p->N, p->L, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  launch_fold(false, false, (const double2*)gfold, p->bufG, p->L, p->P, p->ldw, spin, 0,
+              p->strideG, 1, st);
   LAUNCHED(p);
-  a.gf = p->bufG;
+  FwdArgs a = fwd_args(p, spin);
   a.out = (double2*)R;
   a.out_mode = 1;
   // entries |m| > l stay zero, as in the reference's np.zeros output
-  CU(cudaMemsetAsync(R, 0, sizeof(double2) * (size_t)p->L * p->N, (cudaStream_t)stream));
-  launch_forward_core(a, p->ntiles_fwd, 1, false, (cudaStream_t)stream);
+  CU(cudaMemsetAsync(R, 0, sizeof(double2) * (size_t)p->L * p->N, st));
+  launch_forward_core(a, p->ntiles_fwd, 1, false, st);
   LAUNCHED(p);
   return MWSHT_OK;
 }
@@ -761,14 +790,15 @@ int mwsht_flm_core_real(mwsht_plan* p, const void* gfold, int use_trapani, void*
   (void)use_trapani;
   std::lock_guard<std::mutex> lk(p->mu);
   p->own_launches = p->cufft_launches = 0;
-  FwdArgs a = fwd_args(p, 0);
-  launch_transpose((const double2*)gfold, p->bufG, p->L, p->L, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  launch_fold(true, false, (const double2*)gfold, p->bufG, p->L, p->P, p->ldw, 0, 0, p->strideG,
+              1, st);
   LAUNCHED(p);
-  a.gf = p->bufG;
+  FwdArgs a = fwd_args(p, 0);
   a.out = (double2*)R;
   a.out_mode = 1;
-  CU(cudaMemsetAsync(R, 0, sizeof(double2) * (size_t)p->L * p->L, (cudaStream_t)stream));
-  launch_forward_core(a, p->ntiles_fwd, 1, true, (cudaStream_t)stream);
+  CU(cudaMemsetAsync(R, 0, sizeof(double2) * (size_t)p->L * p->L, st));
+  launch_forward_core(a, p->ntiles_fwd, 1, true, st);
   LAUNCHED(p);
   return MWSHT_OK;
 }
@@ -779,10 +809,8 @@ int mwsht_forward_stages_z(mwsht_plan* p, const void* samples, void* gfold, int 
   if ((rc = check_plan(p)) || (rc = check_spin(p, spin))) return rc;
   std::lock_guard<std::mutex> lk(p->mu);
   p->own_launches = p->cufft_launches = 0;
-  if ((rc = forward_stages(p, 1, samples, false, spin, p->bufG, (long long)p->N * p->L,
-                           (cudaStream_t)stream)))
-    return rc;
-  launch_transpose(p->bufG, (double2*)gfold, p->L, p->N, (cudaStream_t)stream);
+  if ((rc = forward_stages(p, 1, samples, false, spin, (cudaStream_t)stream))) return rc;
+  launch_T2_to_fold(false, p->bufG, (double2*)gfold, p->L, p->ldw, (cudaStream_t)stream);
   LAUNCHED(p);
   return MWSHT_OK;
 }

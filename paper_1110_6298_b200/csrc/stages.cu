@@ -81,39 +81,115 @@ __global__ void k_mul_spectrum(double2* __restrict__ C, const double2* __restric
   }
 }
 
-// Forward: circular correlation output -> m'-folded plane (mw.py:251, 273-285, 504-511),
-// written transposed for the core's bulk copies: gfT[j][r] (rows = orders r).
-// G(m') = C[r][3L-3+m'];  gf[r][0] = G(0), gf[r][j] = G(j) + s_r G(-j),
-// s_r = (-1)^(m+s) (complex, m = r-(L-1)) or (-1)^r (real).
-template <bool REAL>
-__global__ void k_fold_T(const double2* __restrict__ C, double2* __restrict__ gfT, int L, int P,
-                         int spin, long long c_stride, long long g_stride) {
+// Forward: folded plane in the core's staging layout (mw.py:251, 273-285, 504-511):
+//   gf[r][j] = G_r(j) + s_r G_r(-j)  (j = m' >= 0; gf[r][0] = G_r(0)), G_r(m') = C[r][3L-3+m'],
+//   s_r = (-1)^(m+s) (complex, m = r-(L-1)) or (-1)^r (real),
+// written transposed and split by the sign of m, zero-padded to ldw columns:
+//   gfT[j][m] = gf[row(+m)][j],  gfT[L*ldw + j*ldw + m] = (-1)^j gf[row(-m)][j].
+// SRC_CONV: read G from the correlation rows C (length P); else read an
+// already folded (rows x L) plane (kernel-level hook input).
+template <bool REAL, bool SRC_CONV>
+__global__ void k_fold_T2(const double2* __restrict__ src, double2* __restrict__ gfT, int L, int P,
+                          int ldw, int spin, long long s_stride, long long g_stride) {
   __shared__ double2 tile[32][33];
-  const int rows = REAL ? L : 2 * L - 1;
-  const int jb = blockIdx.x * 32, rb = blockIdx.y * 32;
-  const double2* c = C + (long long)blockIdx.z * c_stride;
-  double2* g = gfT + (long long)blockIdx.z * g_stride;
+  const int jb = blockIdx.x * 32, mb = blockIdx.y * 32;
+  const int map = REAL ? blockIdx.z : (blockIdx.z >> 1);
+  const int neg = REAL ? 0 : (blockIdx.z & 1);
+  const double2* c = src + (long long)map * s_stride;
+  double2* g = gfT + (long long)map * g_stride + (neg ? (long long)L * ldw : 0);
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int o = 3 * L - 3;
   for (int k = ty; k < 32; k += 8) {
-    const int r = rb + k, j = jb + tx;
+    const int m = mb + k, j = jb + tx;
     double2 v = make_double2(0.0, 0.0);
-    if (r < rows && j < L) {
-      const double2* row = c + (long long)r * P;
-      v = row[o + j];
-      if (j > 0) {
-        const int m = REAL ? r : r - (L - 1);
-        const double sr = ((m + (REAL ? 0 : spin)) & 1) ? -1.0 : 1.0;
-        const double2 u = row[o - j];
-        v = make_double2(v.x + sr * u.x, v.y + sr * u.y);
+    if (m < L && j < L) {
+      const int r = REAL ? m : (neg ? L - 1 - m : L - 1 + m);
+      if (SRC_CONV) {
+        const double2* row = c + (long long)r * P;
+        v = row[o + j];
+        if (j > 0) {
+          const int mm = REAL ? r : r - (L - 1);
+          const double sr = ((mm + (REAL ? 0 : spin)) & 1) ? -1.0 : 1.0;
+          const double2 u = row[o - j];
+          v = make_double2(v.x + sr * u.x, v.y + sr * u.y);
+        }
+      } else {
+        v = c[(long long)r * L + j];
       }
+      if (neg && (j & 1)) v = make_double2(-v.x, -v.y);
     }
     tile[k][tx] = v;
   }
   __syncthreads();
   for (int k = ty; k < 32; k += 8) {
-    const int j = jb + k, r = rb + tx;
-    if (j < L && r < rows) g[(long long)j * rows + r] = tile[tx][k];
+    const int j = jb + k, m = mb + tx;
+    if (j < L && m < ldw) g[(long long)j * ldw + m] = tile[tx][k];
+  }
+}
+
+// Hook output: staging layout -> folded plane (N x L) (complex) / (L x L) (real).
+template <bool REAL>
+__global__ void k_T2_to_fold(const double2* __restrict__ gfT, double2* __restrict__ gf, int L,
+                             int ldw) {
+  __shared__ double2 tile[32][33];
+  const int mb = blockIdx.x * 32, jb = blockIdx.y * 32;
+  const int neg = REAL ? 0 : blockIdx.z;
+  const double2* g = gfT + (neg ? (long long)L * ldw : 0);
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int k = ty; k < 32; k += 8) {
+    const int j = jb + k, m = mb + tx;
+    double2 v = make_double2(0.0, 0.0);
+    if (j < L && m < L) {
+      v = g[(long long)j * ldw + m];
+      if (neg && (j & 1)) v = make_double2(-v.x, -v.y);
+    }
+    tile[k][tx] = v;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int m = mb + k, j = jb + tx;
+    if (m < L && j < L && !(neg && m == 0)) {
+      const int r = REAL ? m : (neg ? L - 1 - m : L - 1 + m);
+      gf[(long long)r * L + j] = tile[tx][k];
+    }
+  }
+}
+
+// Inverse: coefficients -> the core's pre-scaled staging rows (mw.py:390-392
+// unflatten + the c_l u_l(m) column factor of the l-recursion):
+//   gp[l*ldw+m] = c_l u_l(m) f_{l,m},  gn[l*ldw+m] = (-1)^l c_l u_l(m) f_{l,-m},
+//   u_l(m) = A(l-m) A(l+m), zero for m > l.
+// in_mode 0: flat l(l+1)+m; 1: table (L, N) column L-1+m (real: (L, L) column m).
+template <bool REAL>
+__global__ void k_inv_prescale(const double2* __restrict__ in, int in_mode,
+                               const double* __restrict__ cl, const double* __restrict__ A, int L,
+                               int ldw, double2* __restrict__ gp, long long in_stride,
+                               long long g_stride) {
+  const int l = blockIdx.y;
+  const int N = 2 * L - 1;
+  const double2* f = in + (long long)blockIdx.z * in_stride;
+  double2* p = gp + (long long)blockIdx.z * g_stride;
+  double2* n = p + (long long)L * ldw;
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < ldw; m += gridDim.x * blockDim.x) {
+    double2 vp = make_double2(0.0, 0.0), vn = vp;
+    if (m <= l) {
+      const double u = cl[l] * A[l - m] * A[l + m];
+      double2 fp, fn;
+      if (REAL) {
+        fp = in_mode == 0 ? f[(long long)l * (l + 1) + m] : f[(long long)l * L + m];
+        fn = fp;
+      } else if (in_mode == 0) {
+        fp = f[(long long)l * (l + 1) + m];
+        fn = f[(long long)l * (l + 1) - m];
+      } else {
+        fp = f[(long long)l * N + (L - 1 + m)];
+        fn = f[(long long)l * N + (L - 1 - m)];
+      }
+      vp = cscale(fp, u);
+      vn = cscale(fn, (l & 1) ? -u : u);
+    }
+    p[(long long)l * ldw + m] = vp;
+    if (!REAL) n[(long long)l * ldw + m] = vn;
   }
 }
 
@@ -225,14 +301,40 @@ void launch_mul_spectrum(double2* C, const double2* W, int P, long long nrows, c
   k_mul_spectrum<<<(unsigned)blocks, 256, 0, st>>>(C, W, P, nrows);
 }
 
-void launch_fold(bool real, const double2* C, double2* gfT, int L, int P, int spin, long long cs,
-                 long long gs, int nm, cudaStream_t st) {
-  const int rows = real ? L : 2 * L - 1;
-  dim3 grid((L + 31) / 32, (rows + 31) / 32, nm), block(32, 8);
+void launch_fold(bool real, bool from_conv, const double2* src, double2* gfT, int L, int P,
+                 int ldw, int spin, long long ss, long long gs, int nm, cudaStream_t st) {
+  dim3 grid((L + 31) / 32, ldw / 32, real ? nm : 2 * nm), block(32, 8);
+  if (real) {
+    if (from_conv)
+      k_fold_T2<true, true><<<grid, block, 0, st>>>(src, gfT, L, P, ldw, spin, ss, gs);
+    else
+      k_fold_T2<true, false><<<grid, block, 0, st>>>(src, gfT, L, P, ldw, spin, ss, gs);
+  } else {
+    if (from_conv)
+      k_fold_T2<false, true><<<grid, block, 0, st>>>(src, gfT, L, P, ldw, spin, ss, gs);
+    else
+      k_fold_T2<false, false><<<grid, block, 0, st>>>(src, gfT, L, P, ldw, spin, ss, gs);
+  }
+}
+
+void launch_T2_to_fold(bool real, const double2* gfT, double2* gf, int L, int ldw,
+                       cudaStream_t st) {
+  dim3 grid((L + 31) / 32, (L + 31) / 32, real ? 1 : 2), block(32, 8);
   if (real)
-    k_fold_T<true><<<grid, block, 0, st>>>(C, gfT, L, P, spin, cs, gs);
+    k_T2_to_fold<true><<<grid, block, 0, st>>>(gfT, gf, L, ldw);
   else
-    k_fold_T<false><<<grid, block, 0, st>>>(C, gfT, L, P, spin, cs, gs);
+    k_T2_to_fold<false><<<grid, block, 0, st>>>(gfT, gf, L, ldw);
+}
+
+void launch_inv_prescale(bool real, const double2* in, int in_mode, const double* cl,
+                         const double* A, int L, int ldw, double2* gp, long long is, long long gs,
+                         int nm, cudaStream_t st) {
+  const int threads = 128;
+  dim3 grid((ldw + threads - 1) / threads, L, nm);
+  if (real)
+    k_inv_prescale<true><<<grid, threads, 0, st>>>(in, in_mode, cl, A, L, ldw, gp, is, gs);
+  else
+    k_inv_prescale<false><<<grid, threads, 0, st>>>(in, in_mode, cl, A, L, ldw, gp, is, gs);
 }
 
 void launch_transpose(const double2* in, double2* out, int rows, int cols, cudaStream_t st) {
