@@ -1,0 +1,97 @@
+"""The oracle (oracle/, a CPU restatement of the reference) pinned against the
+reference's own outputs in tests/golden/ (produced by make_golden.py from the
+reference).  CPU only."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden_cfg
+from helpers import SMALL_CASES, checksums, max_abs, random_signal
+
+from oracle import mw_oracle as O
+
+
+@pytest.mark.parametrize("rec", ["trapani", "risbo"])
+@pytest.mark.parametrize("L,spin", SMALL_CASES)
+def test_oracle_reproduces_reference_small(golden_small, L, spin, rec):
+    key = f"L{L}_s{spin}_{rec}"
+    v = O.gaussian_coeffs(L, spin, L + abs(spin))
+    sig = O.inverse(v, L, spin, rec)
+    assert max_abs(sig, golden_small[key + "_samples"]) == 0.0
+    back = O.forward(sig, L, spin, rec)
+    assert max_abs(back, golden_small[key + "_back"]) == 0.0
+    raw = random_signal(L, spin, L + abs(spin))
+    assert max_abs(O.forward(raw, L, spin, rec), golden_small[key + "_fwdraw"]) == 0.0
+
+
+@pytest.mark.parametrize("spin", [0, 2, -1])
+@pytest.mark.parametrize("rec", ["trapani", "risbo"])
+def test_oracle_kernels_bit_identical(golden_small, spin, rec):
+    L = 9
+    key = f"k9_s{spin}_{rec}"
+    cl = np.sqrt((2.0 * np.arange(L) + 1.0) / (4.0 * math.pi))
+    tr = rec == "trapani"
+    assert max_abs(O.fmm_core(golden_small[key + "_flm2d"], cl, L, spin, tr),
+                   golden_small[key + "_fmm"]) == 0.0
+    assert max_abs(O.flm_core(golden_small[key + "_gfold"], L, spin, tr),
+                   golden_small[key + "_flm"]) == 0.0
+
+
+def test_oracle_real_kernels(golden_small):
+    cl = np.sqrt((2.0 * np.arange(8) + 1.0) / (4.0 * math.pi))
+    assert max_abs(O.fmm_core_real(golden_small["k8real_in"], cl, 8, True),
+                   golden_small["k8real_fmm"]) == 0.0
+    assert max_abs(O.flm_core_real(golden_small["k8real_gf"], 8, True),
+                   golden_small["k8real_flm"]) == 0.0
+
+
+def test_oracle_real_path(golden_small):
+    v = O.gaussian_real_coeffs(16, 6)
+    sig = O.inverse_real(v, 16)
+    assert max_abs(sig, golden_small["real16_samples"]) == 0.0
+    assert max_abs(O.forward_real(sig, 16), golden_small["real16_back"]) == 0.0
+
+
+@pytest.mark.parametrize("name", ["L64_s0_trapani", "L256_s2_trapani", "L256_s-2_trapani"])
+def test_oracle_configs(name):
+    g = golden_cfg(name)
+    L, spin = int(g["L"]), int(g["spin"])
+    v = O.gaussian_coeffs(L, spin, int(g["seed"]))
+    np.testing.assert_allclose(checksums(v), g["input_checksums"], rtol=1e-14)
+    sig = O.inverse(v, L, spin, threads=4)
+    assert max_abs(sig.reshape(-1)[g["samples_idx"]], g["samples_sub"]) == 0.0
+    back = O.forward(sig, L, spin, threads=4)
+    assert max_abs(back[g["back_idx"]], g["back_sub"]) == 0.0
+
+
+def test_oracle_threads_do_not_change_bits():
+    L, s = 60, 1
+    rng = np.random.default_rng(0)
+    flm2d = rng.standard_normal((L, 2 * L - 1)) + 1j * rng.standard_normal((L, 2 * L - 1))
+    gf = rng.standard_normal((2 * L - 1, L)) + 1j * rng.standard_normal((2 * L - 1, L))
+    cl = O.cl_table(L)
+    for rec in (True, False):
+        a = O.fmm_core(flm2d, cl, L, s, rec, threads=1)
+        b = O.fmm_core(flm2d, cl, L, s, rec, threads=5)
+        assert max_abs(a, b) == 0.0
+        assert max_abs(O.flm_core(gf, L, s, rec, threads=1),
+                       O.flm_core(gf, L, s, rec, threads=3)) == 0.0
+
+
+def test_golden_inputs_regenerate():
+    # the config inputs are regenerated from seeds on the GPU box: pin the generator
+    for name in ("L64_s0_trapani", "L256_s2_trapani", "L1024_s0_trapani_real",
+                 "L1100_s0_risbo"):
+        g = golden_cfg(name)
+        L, spin = int(g["L"]), int(g["spin"])
+        v = (O.gaussian_real_coeffs(L, int(g["seed"])) if bool(g["real"])
+             else O.gaussian_coeffs(L, spin, int(g["seed"])))
+        np.testing.assert_allclose(checksums(v), g["input_checksums"], rtol=1e-13)
+
+
+def test_real_coefficients_are_real_symmetric():
+    v = O.gaussian_real_coeffs(12, 3)
+    worst, tol = O.reality_residual(v, 12)
+    assert worst <= tol
