@@ -63,11 +63,14 @@ _SIGS = {
 EXPORTED = tuple(_SIGS)
 
 
-def load(path=LIB_PATH):
-    """Load (once) and return the native library; raises DeviceError if absent."""
+def load(path=None):
+    """Load (once) and return the native library; raises DeviceError if absent.
+
+    MWSHT_LIB overrides the in-tree path (used to A/B kernel variants)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("MWSHT_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise DeviceError(
             f"native library {path} is missing: build it with "

@@ -1,5 +1,4 @@
 // Plan, tables and the extern "C" entry points of libmwsht.so (include/mwsht.h).
-#include <cufft.h>
 #include <float.h>
 #include <math.h>
 #include <stdio.h>
@@ -34,6 +33,24 @@ void launch_untranspose(bool real, const double2* S, double2* Out, int L, int N,
                         long long os, int nm, cudaStream_t st);
 void launch_reality(const double2* f, int L, unsigned long long* worst, unsigned long long* peak,
                     cudaStream_t st);
+namespace fft {
+struct FftArgs {
+  int L, N, M, H, logH, ldw, spin;
+  const double2* tw;
+  const double2* chirp;
+  const double2* specf;
+  const double2* speci;
+  const double2* specw;
+  const double2* rho;
+  double2* scratch;
+  const void* in;
+  void* out;
+  long long in_stride, out_stride;
+  int nrows, nmaps;
+};
+}  // namespace fft
+void fft_launch(int which, bool real, const fft::FftArgs& a, int nsm, cudaStream_t st);
+void fft_spectrum(const fft::FftArgs& a, const double2* kern, double2* spec, cudaStream_t st);
 }  // namespace mwsht
 
 using namespace mwsht;
@@ -52,15 +69,6 @@ static int fail(int code, const char* what, const char* detail) {
     cudaError_t e_ = (call);                                                       \
     if (e_ != cudaSuccess) return fail(MWSHT_E_CUDA, #call, cudaGetErrorString(e_)); \
   } while (0)
-#define FFT(call)                                                                  \
-  do {                                                                             \
-    cufftResult r_ = (call);                                                       \
-    if (r_ != CUFFT_SUCCESS) {                                                     \
-      char b_[32];                                                                 \
-      snprintf(b_, sizeof b_, "cufftResult %d", (int)r_);                          \
-      return fail(MWSHT_E_CUFFT, #call, b_);                                       \
-    }                                                                              \
-  } while (0)
 #define LAUNCHED(p)                                             \
   do {                                                          \
     cudaError_t e_ = cudaGetLastError();                        \
@@ -68,7 +76,6 @@ static int fail(int code, const char* what, const char* detail) {
     (p)->own_launches++;                                        \
   } while (0)
 
-enum FftKind { F_PHI_Z = 0, F_PHI_D2Z, F_PHI_Z2D, F_ROWN, F_ROWP, F_ROWP_HALF, F_WSPEC };
 
 struct SpinTab {
   double2* rowinv = nullptr;  // [l*ldw + m'] = (kap_l C_l(m'), W_l(m'))
@@ -76,7 +83,7 @@ struct SpinTab {
 };
 
 struct mwsht_plan {
-  int L = 0, N = 0, P = 0, device = 0, max_batch = 1;
+  int L = 0, N = 0, device = 0, max_batch = 1;
   int ldw = 0;  // DW tables' leading dimension: L rounded up to the 64-wide tile
   DevTables tabs{};
   std::vector<void*> allocs;
@@ -84,14 +91,14 @@ struct mwsht_plan {
   std::map<int, SpinTab> spins;
   int2 *tiles_inv = nullptr, *tiles_fwd = nullptr;
   int ntiles_inv = 0, ntiles_fwd = 0;
-  double2* wspec = nullptr;
-  double2 *bufA = nullptr, *bufB = nullptr, *bufC = nullptr, *bufG = nullptr;
-  long long strideA = 0, strideB = 0, strideC = 0, strideG = 0;
-  std::map<std::pair<int, int>, cufftHandle> ffts;
-  void* fft_work = nullptr;
-  size_t fft_work_size = 0;
+  // fused FFT engine (fft.cu): M-point FFT-convolutions in H = M/2 smem halves
+  int M = 0, H = 0, logH = 0, nsm = 0;
+  double2 *tw = nullptr, *chirp = nullptr, *specf = nullptr, *speci = nullptr, *specw = nullptr,
+          *rho = nullptr, *scratch = nullptr;
+  double2 *bufA = nullptr, *bufB = nullptr, *bufG = nullptr;
+  long long strideA = 0, strideB = 0, strideG = 0;
   unsigned long long* red = nullptr;  // 2 slots for the reality check
-  int own_launches = 0, cufft_launches = 0;
+  int own_launches = 0;
   bool timing = false;
   cudaEvent_t ev[2][3] = {};  // [forward|inverse][start, core start, core end]
   double* colc = nullptr;  // [l*ldw + m] = C_l(m)
@@ -132,15 +139,6 @@ static void host_parallel(int n, F f) {
   for (auto& x : th) x.join();
 }
 
-static int smooth_len(int n) {
-  // smallest 2^a 3^b 5^c 7^d >= n (cuFFT-friendly)
-  for (int m = n;; m++) {
-    int x = m;
-    for (int q : {2, 3, 5, 7})
-      while (x % q == 0) x /= q;
-    if (x == 1) return m;
-  }
-}
 
 // ------------------------------------------------------------- tables
 static int build_tables(mwsht_plan* p) {
@@ -324,96 +322,103 @@ static int build_tiles(mwsht_plan* p) {
   return MWSHT_OK;
 }
 
-// cuFFT plan cache keyed by (kind, nmaps); all plans share one work area.
-static int get_fft(mwsht_plan* p, int kind, int nm, cufftHandle* out) {
-  auto key = std::make_pair(kind, nm);
-  auto it = p->ffts.find(key);
-  if (it != p->ffts.end()) {
-    *out = it->second;
-    return MWSHT_OK;
-  }
-  const int L = p->L, N = p->N, P = p->P;
-  cufftHandle h;
-  FFT(cufftCreate(&h));
-  FFT(cufftSetAutoAllocation(h, 0));
-  size_t ws = 0;
-  int n1[1];
-  switch (kind) {
-    case F_PHI_Z:
-      n1[0] = N;
-      FFT(cufftMakePlanMany(h, 1, n1, nullptr, 1, N, nullptr, 1, N, CUFFT_Z2Z, L * nm, &ws));
-      break;
-    case F_PHI_D2Z:
-      n1[0] = N;
-      FFT(cufftMakePlanMany(h, 1, n1, nullptr, 1, N, nullptr, 1, L, CUFFT_D2Z, L * nm, &ws));
-      break;
-    case F_PHI_Z2D:
-      n1[0] = N;
-      FFT(cufftMakePlanMany(h, 1, n1, nullptr, 1, L, nullptr, 1, N, CUFFT_Z2D, L * nm, &ws));
-      break;
-    case F_ROWN:
-      n1[0] = N;
-      FFT(cufftMakePlanMany(h, 1, n1, nullptr, 1, N, nullptr, 1, N, CUFFT_Z2Z, N * nm, &ws));
-      break;
-    case F_ROWP:
-      n1[0] = P;
-      FFT(cufftMakePlanMany(h, 1, n1, nullptr, 1, P, nullptr, 1, P, CUFFT_Z2Z, N * nm, &ws));
-      break;
-    case F_ROWP_HALF:
-      n1[0] = P;
-      FFT(cufftMakePlanMany(h, 1, n1, nullptr, 1, P, nullptr, 1, P, CUFFT_Z2Z, L * nm, &ws));
-      break;
-    case F_WSPEC:
-      n1[0] = P;
-      FFT(cufftMakePlanMany(h, 1, n1, nullptr, 1, P, nullptr, 1, P, CUFFT_Z2Z, 1, &ws));
-      break;
-  }
-  if (ws > p->fft_work_size) {
-    if (p->fft_work) {
-      CU(cudaDeviceSynchronize());
-      auto itp = std::find(p->allocs.begin(), p->allocs.end(), p->fft_work);
-      if (itp != p->allocs.end()) p->allocs.erase(itp);
-      cudaFree(p->fft_work);
-      p->bytes -= p->fft_work_size;
-      p->fft_work = nullptr;
-    }
-    int rc = dev_alloc(p, &p->fft_work, ws);
-    if (rc) return rc;
-    p->fft_work_size = ws;
-    for (auto& kv : p->ffts) FFT(cufftSetWorkArea(kv.second, p->fft_work));
-  }
-  FFT(cufftSetWorkArea(h, p->fft_work));
-  p->ffts[key] = h;
-  *out = h;
-  return MWSHT_OK;
+// Fused-FFT tables (fft.cu): quarter twiddles w_M^j, chirp c[n] = e^{i pi n^2/N},
+// spectra (half-split DIF of the Bluestein kernels c, conj c and of the
+// weight-correlation kernel K'[d mod M] = 2 pi w(-d), |d| <= 2L-2,
+// quadrature.py:66-74, mw.py:237-238), and the forward theta glue
+// rho[k] = conj(c[k]) e^{-i f(k) pi/N} / (2 pi N M), f(k) = k (k < L), k - N.
+static fft::FftArgs fft_args(mwsht_plan* p) {
+  fft::FftArgs a{};
+  a.L = p->L;
+  a.N = p->N;
+  a.M = p->M;
+  a.H = p->H;
+  a.logH = p->logH;
+  a.ldw = p->ldw;
+  a.tw = p->tw;
+  a.chirp = p->chirp;
+  a.specf = p->specf;
+  a.speci = p->speci;
+  a.specw = p->specw;
+  a.rho = p->rho;
+  a.scratch = p->scratch;
+  a.nmaps = 1;
+  return a;
 }
 
-static int build_wspec(mwsht_plan* p) {
-  const int L = p->L, P = p->P;
-  std::vector<double2> w(P, make_double2(0.0, 0.0));
-  // w_rev[i] = w(2L-2-i), i < 4L-3 (mw.py:237, quadrature.py:66-74)
-  for (int i = 0; i < 4 * L - 3; i++) {
-    const long long k = 2LL * L - 2 - i;
+static int build_fft_tables(mwsht_plan* p) {
+  typedef long double ld;
+  const int L = p->L, N = p->N;
+  int M = 8;
+  while (M < 4 * L - 3 || M < 2 * N - 1) M <<= 1;
+  p->M = M;
+  p->H = M / 2;
+  p->logH = 0;
+  while ((1 << p->logH) < p->H) p->logH++;
+  if (p->H > 8192) return fail(MWSHT_E_BAND_LIMIT, "plan_create", "fused FFT engine supports L <= 4096");
+  const ld PI = 3.141592653589793238462643383279502884L;
+  std::vector<double2> tw(M / 4 + 1), ch(N), rho(N), kf(M, make_double2(0, 0)), ki(kf), kw(kf);
+  for (int j = 0; j <= M / 4; j++) {
+    const ld a = -2.0L * PI * (ld)j / (ld)M;
+    tw[j] = make_double2((double)cosl(a), (double)sinl(a));
+  }
+  tw[0] = make_double2(1.0, 0.0);
+  tw[M / 4] = make_double2(0.0, -1.0);
+  std::vector<ld> cr(N), ci(N);
+  for (int n = 0; n < N; n++) {
+    const long long e = ((long long)n * n) % (2LL * N);  // c[n] = e^{i pi e/N}
+    const ld a = PI * (ld)e / (ld)N;
+    cr[n] = cosl(a);
+    ci[n] = sinl(a);
+    ch[n] = make_double2((double)cr[n], (double)ci[n]);
+  }
+  for (int k = 0; k < N; k++) {
+    const int f = k < L ? k : k - N;
+    const ld a = -PI * (ld)f / (ld)N;  // tau phase
+    const ld sc = 1.0L / (2.0L * PI * (ld)N * (ld)M);
+    const ld tr = cosl(a) * sc, ti = sinl(a) * sc;
+    // conj(c) * tau
+    rho[k] = make_double2((double)(cr[k] * tr + ci[k] * ti), (double)(cr[k] * ti - ci[k] * tr));
+  }
+  for (int j = -(N - 1); j <= N - 1; j++) {
+    const int n = j < 0 ? -j : j;
+    const int idx = (j + M) % M;
+    kf[idx] = ch[n];
+    ki[idx] = make_double2(ch[n].x, -ch[n].y);
+  }
+  for (long long d = -(2LL * L - 2); d <= 2LL * L - 2; d++) {
+    const long long k = -d;  // K'[d] = 2 pi w(-d)
     double2 v = make_double2(0.0, 0.0);
     if (k == 1)
-      v.y = 0.5 * 3.141592653589793;
+      v.y = (double)(PI * PI);  // 2 pi * (i pi/2)
     else if (k == -1)
-      v.y = -0.5 * 3.141592653589793;
+      v.y = (double)(-PI * PI);
     else if ((k & 1) == 0)
-      v.x = 2.0 / (1.0 - (double)k * (double)k);
-    w[i] = v;
+      v.x = (double)(2.0L * PI * 2.0L / (1.0L - (ld)k * (ld)k));
+    kw[(d + M) % M] = v;
   }
   int rc;
-  if ((rc = upload(p, &p->wspec, w))) return rc;
-  cufftHandle h;
-  if ((rc = get_fft(p, F_WSPEC, 1, &h))) return rc;
-  FFT(cufftExecZ2Z(h, (cufftDoubleComplex*)p->wspec, (cufftDoubleComplex*)p->wspec, CUFFT_FORWARD));
+  if ((rc = upload(p, &p->tw, tw)) || (rc = upload(p, &p->chirp, ch)) ||
+      (rc = upload(p, &p->rho, rho)))
+    return rc;
+  double2 *dkf, *dki, *dkw;
+  if ((rc = upload(p, &dkf, kf)) || (rc = upload(p, &dki, ki)) || (rc = upload(p, &dkw, kw)))
+    return rc;
+  if ((rc = dev_alloc(p, (void**)&p->specf, sizeof(double2) * M)) ||
+      (rc = dev_alloc(p, (void**)&p->speci, sizeof(double2) * M)) ||
+      (rc = dev_alloc(p, (void**)&p->specw, sizeof(double2) * M)))
+    return rc;
+  fft::FftArgs a = fft_args(p);
+  fft_spectrum(a, dkf, p->specf, 0);
+  fft_spectrum(a, dki, p->speci, 0);
+  fft_spectrum(a, dkw, p->specw, 0);
+  CU(cudaGetLastError());
   CU(cudaDeviceSynchronize());
-  std::vector<double2> hw(P);
-  CU(cudaMemcpy(hw.data(), p->wspec, P * sizeof(double2), cudaMemcpyDeviceToHost));
-  const double sc = 2.0 * 3.141592653589793 / (double)P;  // 2pi (mw.py:238) and the 1/P of the inverse FFT
-  for (auto& v : hw) v = make_double2(v.x * sc, v.y * sc);
-  CU(cudaMemcpy(p->wspec, hw.data(), P * sizeof(double2), cudaMemcpyHostToDevice));
+  int dev;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, dev));
+  if ((rc = dev_alloc(p, (void**)&p->scratch, sizeof(double2) * 2 * (size_t)p->H * p->nsm)))
+    return rc;
   return MWSHT_OK;
 }
 
@@ -461,48 +466,29 @@ static FwdArgs fwd_args(mwsht_plan* p, int spin) {
   return a;
 }
 
-// samples (L,N) -> folded plane in the forward core's staging layout (bufG)
+// samples (L,N) -> folded plane in the forward core's staging layout (bufG):
+// fused phi DFT (k_phi_fwd: mw.py:149-158 / :489) writing the transposed ring
+// spectra AT, then the fused theta stage (k_theta_fwd: extension, DFT + twist,
+// weight correlation, m' fold: mw.py:161-285).
 static int forward_stages(mwsht_plan* p, int nm, const void* samples, bool real, int spin,
                           cudaStream_t st) {
-  const int L = p->L, N = p->N, P = p->P;
-  cufftHandle hphi, hrow, hconv;
-  int rc;
-  if ((rc = get_fft(p, real ? F_PHI_D2Z : F_PHI_Z, nm, &hphi))) return rc;
-  if ((rc = get_fft(p, real ? F_PHI_Z : F_ROWN, nm, &hrow))) return rc;
-  if ((rc = get_fft(p, real ? F_ROWP_HALF : F_ROWP, nm, &hconv))) return rc;
-  FFT(cufftSetStream(hphi, st));
-  FFT(cufftSetStream(hrow, st));
-  FFT(cufftSetStream(hconv, st));
-  const int rows = real ? L : N;
-  // 1. phi FFT (mw.py:149-158 / :489)
-  if (real)
-    FFT(cufftExecD2Z(hphi, (cufftDoubleReal*)samples, (cufftDoubleComplex*)p->bufA));
-  else
-    FFT(cufftExecZ2Z(hphi, (cufftDoubleComplex*)samples, (cufftDoubleComplex*)p->bufA,
-                     CUFFT_FORWARD));
-  p->cufft_launches++;
-  // 2. periodic extension + transpose + 2pi/N (mw.py:161-177)
-  const long long sA = real ? (long long)L * L : (long long)L * N;
-  launch_extend_transpose(real, p->bufA, p->bufB, L, N, spin, 2.0 * 3.141592653589793 / N, sA,
-                          (long long)rows * N, nm, st);
+  const int L = p->L, N = p->N;
+  fft::FftArgs a = fft_args(p);
+  a.spin = spin;
+  a.nmaps = nm;
+  a.nrows = L;
+  a.in = samples;
+  a.in_stride = (long long)L * N;  // elements (double for real, double2 for complex)
+  a.out = p->bufA;
+  a.out_stride = p->strideA;
+  fft_launch(0, real, a, p->nsm, st);
   LAUNCHED(p);
-  // 3. theta FFT over t (mw.py:190)
-  FFT(cufftExecZ2Z(hrow, (cufftDoubleComplex*)p->bufB, (cufftDoubleComplex*)p->bufB, CUFFT_FORWARD));
-  p->cufft_launches++;
-  // 4. twist + scale + zero pad to P (mw.py:191, 250)
-  launch_pad_twist(p->bufB, p->bufC, rows, L, N, P, (long long)rows * N, (long long)rows * P, nm,
-                   st);
-  LAUNCHED(p);
-  // 5. correlation with w by FFT at P >= 4L-3 (mw.py:244-251)
-  FFT(cufftExecZ2Z(hconv, (cufftDoubleComplex*)p->bufC, (cufftDoubleComplex*)p->bufC, CUFFT_FORWARD));
-  p->cufft_launches++;
-  launch_mul_spectrum(p->bufC, p->wspec, P, (long long)rows * nm, st);
-  LAUNCHED(p);
-  FFT(cufftExecZ2Z(hconv, (cufftDoubleComplex*)p->bufC, (cufftDoubleComplex*)p->bufC, CUFFT_INVERSE));
-  p->cufft_launches++;
-  // 6. extract + m' fold into the core's layout (mw.py:251, 273-285)
-  launch_fold(real, true, p->bufC, p->bufG, L, P, p->ldw, spin, (long long)rows * P, p->strideG,
-              nm, st);
+  a.nrows = real ? L : N;
+  a.in = p->bufA;
+  a.in_stride = p->strideA;
+  a.out = p->bufG;
+  a.out_stride = p->strideG;
+  fft_launch(1, real, a, p->nsm, st);
   LAUNCHED(p);
   return MWSHT_OK;
 }
@@ -517,7 +503,7 @@ static int do_forward(mwsht_plan* p, int nm, const void* samples, void* flm, int
   if (nm < 1 || nm > p->max_batch) return fail(MWSHT_E_CONTRACT, "nmaps", "exceeds plan max_batch");
   std::lock_guard<std::mutex> lk(p->mu);
   if ((rc = build_spin(p, spin))) return rc;
-  p->own_launches = p->cufft_launches = 0;
+  p->own_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
   const int L = p->L;
   if (p->timing) CU(cudaEventRecord(p->ev[0][0], st));
@@ -543,15 +529,10 @@ static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int
   if (nm < 1 || nm > p->max_batch) return fail(MWSHT_E_CONTRACT, "nmaps", "exceeds plan max_batch");
   std::lock_guard<std::mutex> lk(p->mu);
   if ((rc = build_spin(p, spin))) return rc;
-  p->own_launches = p->cufft_launches = 0;
+  p->own_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
   const int L = p->L, N = p->N;
   const int rows = real ? L : N;
-  cufftHandle hrow, hphi;
-  if ((rc = get_fft(p, real ? F_PHI_Z : F_ROWN, nm, &hrow))) return rc;
-  if ((rc = get_fft(p, real ? F_PHI_Z2D : F_PHI_Z, nm, &hphi))) return rc;
-  FFT(cufftSetStream(hrow, st));
-  FFT(cufftSetStream(hphi, st));
   if (p->timing) CU(cudaEventRecord(p->ev[1][0], st));
   // 0. unflatten + c_l u_l(m) scaling into the core's staging rows (mw.py:390-392)
   launch_inv_prescale(real, (const double2*)flm, 0, p->tabs.cl, p->tabs.A, L, p->ldw, p->bufG,
@@ -566,20 +547,24 @@ static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int
   launch_inverse_core(a, p->ntiles_inv, nm, real, st);
   LAUNCHED(p);
   if (p->timing) CU(cudaEventRecord(p->ev[1][2], st));
-  // 2. theta synthesis (mw.py:446), unnormalised inverse FFT over m'
-  FFT(cufftExecZ2Z(hrow, (cufftDoubleComplex*)p->bufB, (cufftDoubleComplex*)p->bufB, CUFFT_INVERSE));
-  p->cufft_launches++;
-  // 3. keep t < L, transpose to rings, ifftshift over m (mw.py:436-437)
-  const long long sA = real ? (long long)L * L : (long long)L * N;
-  launch_untranspose(real, p->bufB, p->bufA, L, N, (long long)rows * N, sA, nm, st);
+  // 2. theta synthesis (mw.py:441-446), keep t < L, transposed to rings (:436-437)
+  fft::FftArgs f = fft_args(p);
+  f.nmaps = nm;
+  f.nrows = rows;
+  f.in = p->bufB;
+  f.in_stride = (long long)rows * N;
+  f.out = p->bufA;
+  f.out_stride = p->strideA;
+  fft_launch(2, real, f, p->nsm, st);
   LAUNCHED(p);
-  // 4. phi synthesis (mw.py:437-438 / 558)
-  if (real)
-    FFT(cufftExecZ2D(hphi, (cufftDoubleComplex*)p->bufA, (cufftDoubleReal*)samples));
-  else
-    FFT(cufftExecZ2Z(hphi, (cufftDoubleComplex*)p->bufA, (cufftDoubleComplex*)samples,
-                     CUFFT_INVERSE));
-  p->cufft_launches++;
+  // 3. phi synthesis (mw.py:437-438 / 558)
+  f.nrows = L;
+  f.in = p->bufA;
+  f.in_stride = p->strideA;
+  f.out = samples;
+  f.out_stride = (long long)L * N;
+  fft_launch(3, real, f, p->nsm, st);
+  LAUNCHED(p);
   return MWSHT_OK;
 }
 
@@ -623,7 +608,6 @@ int mwsht_plan_create(int L, int device, int max_batch, mwsht_plan** out) {
   }
   p->L = L;
   p->N = 2 * L - 1;
-  p->P = smooth_len(4 * L - 3);
   p->ldw = (L + kTileRows - 1) / kTileRows * kTileRows;
   p->device = device;
   p->max_batch = max_batch;
@@ -632,20 +616,24 @@ int mwsht_plan_create(int L, int device, int max_batch, mwsht_plan** out) {
     delete p;
     return fail(MWSHT_E_CUDA, "cudaSetDevice", cudaGetErrorString(e));
   }
-  const long long L_ = L, N = p->N, P = p->P;
+  const long long L_ = L, N = p->N;
   p->strideA = L_ * N;
   p->strideB = N * N;
-  p->strideC = N * P;
   p->strideG = 2 * L_ * p->ldw;
-  if ((rc = build_tables(p)) || (rc = build_tiles(p)) ||
+  if ((rc = build_tables(p)) || (rc = build_tiles(p)) || (rc = build_fft_tables(p)) ||
       (rc = dev_alloc(p, (void**)&p->bufA, sizeof(double2) * p->strideA * max_batch)) ||
       (rc = dev_alloc(p, (void**)&p->bufB, sizeof(double2) * p->strideB * max_batch)) ||
-      (rc = dev_alloc(p, (void**)&p->bufC, sizeof(double2) * p->strideC * max_batch)) ||
       (rc = dev_alloc(p, (void**)&p->bufG, sizeof(double2) * p->strideG * max_batch)) ||
       (rc = dev_alloc(p, (void**)&p->red, 2 * sizeof(unsigned long long))) ||
-      (rc = build_wspec(p)) || (rc = build_spin(p, 0))) {
+      (rc = build_spin(p, 0))) {
     mwsht_plan_destroy(p);
     return rc;
+  }
+  // the staging buffer's pad columns (m >= L) are read but never written: zero them once
+  e = cudaMemset(p->bufG, 0, sizeof(double2) * p->strideG * max_batch);
+  if (e != cudaSuccess) {
+    mwsht_plan_destroy(p);
+    return fail(MWSHT_E_CUDA, "cudaMemset", cudaGetErrorString(e));
   }
   *out = p;
   return MWSHT_OK;
@@ -655,7 +643,6 @@ int mwsht_plan_destroy(mwsht_plan* p) {
   if (!p) return MWSHT_OK;
   cudaSetDevice(p->device);
   cudaDeviceSynchronize();
-  for (auto& kv : p->ffts) cufftDestroy(kv.second);
   for (auto& d : p->ev)
     for (auto& e : d)
       if (e) cudaEventDestroy(e);
@@ -730,7 +717,7 @@ int mwsht_fmm_core(mwsht_plan* p, const void* flm2d, const double* cl, int spin,
   (void)use_trapani;
   std::lock_guard<std::mutex> lk(p->mu);
   if ((rc = build_spin(p, spin))) return rc;
-  p->own_launches = p->cufft_launches = 0;
+  p->own_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
   launch_inv_prescale(false, (const double2*)flm2d, 1, cl, p->tabs.A, p->L, p->ldw, p->bufG, 0,
                       p->strideG, 1, st);
@@ -749,7 +736,7 @@ int mwsht_fmm_core_real(mwsht_plan* p, const void* flm_half, const double* cl, i
   if ((rc = check_plan(p))) return rc;
   (void)use_trapani;
   std::lock_guard<std::mutex> lk(p->mu);
-  p->own_launches = p->cufft_launches = 0;
+  p->own_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
   launch_inv_prescale(true, (const double2*)flm_half, 1, cl, p->tabs.A, p->L, p->ldw, p->bufG, 0,
                       p->strideG, 1, st);
@@ -769,9 +756,9 @@ int mwsht_flm_core(mwsht_plan* p, const void* gfold, int spin, int use_trapani, 
   (void)use_trapani;
   std::lock_guard<std::mutex> lk(p->mu);
   if ((rc = build_spin(p, spin))) return rc;
-  p->own_launches = p->cufft_launches = 0;
+  p->own_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
-  launch_fold(false, false, (const double2*)gfold, p->bufG, p->L, p->P, p->ldw, spin, 0,
+  launch_fold(false, false, (const double2*)gfold, p->bufG, p->L, 0, p->ldw, spin, 0,
               p->strideG, 1, st);
   LAUNCHED(p);
   FwdArgs a = fwd_args(p, spin);
@@ -789,9 +776,9 @@ int mwsht_flm_core_real(mwsht_plan* p, const void* gfold, int use_trapani, void*
   if ((rc = check_plan(p))) return rc;
   (void)use_trapani;
   std::lock_guard<std::mutex> lk(p->mu);
-  p->own_launches = p->cufft_launches = 0;
+  p->own_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
-  launch_fold(true, false, (const double2*)gfold, p->bufG, p->L, p->P, p->ldw, 0, 0, p->strideG,
+  launch_fold(true, false, (const double2*)gfold, p->bufG, p->L, 0, p->ldw, 0, 0, p->strideG,
               1, st);
   LAUNCHED(p);
   FwdArgs a = fwd_args(p, 0);
@@ -808,7 +795,7 @@ int mwsht_forward_stages_z(mwsht_plan* p, const void* samples, void* gfold, int 
   int rc;
   if ((rc = check_plan(p)) || (rc = check_spin(p, spin))) return rc;
   std::lock_guard<std::mutex> lk(p->mu);
-  p->own_launches = p->cufft_launches = 0;
+  p->own_launches = 0;
   if ((rc = forward_stages(p, 1, samples, false, spin, (cudaStream_t)stream))) return rc;
   launch_T2_to_fold(false, p->bufG, (double2*)gfold, p->L, p->ldw, (cudaStream_t)stream);
   LAUNCHED(p);
@@ -842,7 +829,7 @@ int mwsht_plan_last_timing(mwsht_plan* p, int inverse, float* core_ms, float* st
 int mwsht_plan_last_launches(const mwsht_plan* p, int* own, int* cufft) {
   if (!p) return MWSHT_E_PLAN;
   if (own) *own = p->own_launches;
-  if (cufft) *cufft = p->cufft_launches;
+  if (cufft) *cufft = 0;  // no library FFT launches: the FFT stages are fused kernels
   return MWSHT_OK;
 }
 
