@@ -148,6 +148,29 @@ int mwsht_forward_stages_z(mwsht_plan *plan, const void *samples, void *gfold, i
  * (own kernels only, cuFFT excluded / included). */
 int mwsht_plan_last_launches(const mwsht_plan *plan, int *own, int *cufft);
 
+/* ------------------------------------------------ m-column / ring sharding ----
+ * Stage entry points of ONE complex map split over ranks: a
+ * rank owns the orders m0 <= |m| < m1 (m0, m1 multiples of 32, or m1 = L) and
+ * the rings t0 <= t < t1.  With the l-recursion / Trapani-column cores every
+ * chain is independent, so no Delta halo is exchanged; the only exchange is
+ * one all-to-all transpose of the ring spectra per transform, done by the
+ * caller on its own buffers (paper_1110_6298_b200/shard.py, NCCL):
+ *   forward: shard_forward_phi (rings t0..t1 of `samples_rows` -> columns
+ *            t0..t1 of AT (N x L, row bin(m))) ; all-to-all so that AT holds
+ *            rows bin(+-m), m0 <= |m| < m1, for all t ; shard_forward_rest
+ *            (theta stage + forward core) writes flm[l(l+1)+m] for those m.
+ *   inverse: shard_inverse_front (core + theta synthesis) writes columns
+ *            bin(+-m) of OUT (L x N) ; all-to-all so that OUT holds rows
+ *            t0..t1 ; shard_inverse_phi writes those rings of the samples. */
+int mwsht_shard_forward_phi(mwsht_plan *plan, const void *samples_rows, int t0, int t1, void *AT,
+                            void *stream);
+int mwsht_shard_forward_rest(mwsht_plan *plan, const void *AT, int m0, int m1, int spin, void *flm,
+                             void *stream);
+int mwsht_shard_inverse_front(mwsht_plan *plan, const void *flm, int m0, int m1, int spin,
+                              void *OUT, void *stream);
+int mwsht_shard_inverse_phi(mwsht_plan *plan, const void *OUT, int t0, int t1, void *samples_rows,
+                            void *stream);
+
 /* Per-call event timing of the O(L^3) core kernel (bench / roofline).  When
  * enabled, each transform records CUDA events on its stream around the FFT
  * stages and around the core kernel; last_timing synchronises on them. */

@@ -54,6 +54,10 @@ _SIGS = {
     "mwsht_forward_stages_z": ([_P, _P, _P, _I, _P], _I),
     "mwsht_plan_last_launches": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
     "mwsht_plan_set_timing": ([_P, _I], _I),
+    "mwsht_shard_forward_phi": ([_P, _P, _I, _I, _P, _P], _I),
+    "mwsht_shard_forward_rest": ([_P, _P, _I, _I, _I, _P, _P], _I),
+    "mwsht_shard_inverse_front": ([_P, _P, _I, _I, _I, _P, _P], _I),
+    "mwsht_shard_inverse_phi": ([_P, _P, _I, _I, _P, _P], _I),
     "mwsht_plan_last_timing": ([_P, _I, ctypes.POINTER(ctypes.c_float),
                                 ctypes.POINTER(ctypes.c_float)], _I),
     "mwsht_fp64_probe": ([_I, ctypes.POINTER(ctypes.c_double),

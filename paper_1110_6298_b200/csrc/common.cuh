@@ -123,6 +123,26 @@ struct FwdArgs {
   long long in_stride, out_stride;
 };
 
+namespace fft {
+// Arguments of the fused FFT-stage kernels (fft.cu).
+struct FftArgs {
+  int L, N, M, H, logH, ldw, spin;
+  const double2* tw;      // w_M^j = e^{-2 pi i j/M}, j = 0..M/4 (global; staged to smem)
+  const double2* chirp;   // c[n] = e^{+i pi n^2 / N}, n < N
+  const double2* specf;   // forward Bluestein spectrum, halves [0,H) and [H,2H) (DFT_M of c)
+  const double2* speci;   // inverse Bluestein spectrum (DFT_M of conj c)
+  const double2* specw;   // weight-correlation spectrum (DFT_M of K'), 2pi included
+  const double2* rho;     // forward theta glue: conj(c[k]) tau(f(k)) / M  (k < N)
+  double2* scratch;       // per-CTA L2 scratch: 2H complex per CTA
+  const void* in;         // stage input
+  void* out;              // stage output
+  long long in_stride, out_stride;  // per-map strides (elements)
+  int nrows, nmaps;
+  int m0, m1;  // theta kernels: rows are the orders m with m0 <= |m| < m1 (full: 0, L)
+  int t0;      // phi kernels: rows are the rings t0 .. t0+nrows-1
+};
+}  // namespace fft
+
 }  // namespace mwsht
 
 // ------------------------------------------------------- async bulk copies

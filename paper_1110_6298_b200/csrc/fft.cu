@@ -28,20 +28,14 @@ namespace fft {
 
 constexpr int kT = 512;  // threads per CTA
 
-struct FftArgs {
-  int L, N, M, H, logH, ldw, spin;
-  const double2* tw;      // w_M^j = e^{-2 pi i j/M}, j = 0..M/4 (global; staged to smem)
-  const double2* chirp;   // c[n] = e^{+i pi n^2 / N}, n < N
-  const double2* specf;   // forward Bluestein spectrum, halves [0,H) and [H,2H) (DFT_M of c)
-  const double2* speci;   // inverse Bluestein spectrum (DFT_M of conj c)
-  const double2* specw;   // weight-correlation spectrum (DFT_M of K'), 2pi included
-  const double2* rho;     // forward theta glue: conj(c[k]) tau(f(k)) / M  (k < N)
-  double2* scratch;       // per-CTA L2 scratch: 2H complex per CTA
-  const void* in;         // stage input
-  void* out;              // stage output
-  long long in_stride, out_stride;  // per-map strides (elements)
-  int nrows, nmaps;
-};
+
+
+// i-th order row of an |m| range [m0, m1): +m0..+(m1-1), then -m0..-(m1-1) (m = 0 once)
+__device__ __forceinline__ int row_order(int i, int m0, int m1, bool real) {
+  const int n = m1 - m0;
+  if (real || i < n) return m0 + i;
+  return -(m0 + (i - n) + (m0 == 0 ? 1 : 0));
+}
 
 // XOR swizzle of 16-byte elements inside each 128-byte segment: strided and
 // contiguous radix-R accesses of a warp land on distinct bank groups.
@@ -217,6 +211,9 @@ __device__ __forceinline__ void pass_r(int lr, const double2* tw, const double2*
 // pass, the spectrum multiply and the innermost DIT pass are one register
 // pass, and the last DIT pass hands results to OUT, so the H-point buffer X
 // is touched by 2*(np-1) shared-memory passes instead of 2*np + 2.
+#ifndef MWSHT_FFT_FUSE_IO
+#define MWSHT_FFT_FUSE_IO 0
+#endif
 template <class IN, class OUT>
 __device__ __forceinline__ void conv_half(double2* X, const double2* tw, const double2* S,
                                           const FftArgs& a, IN in, OUT out) {
@@ -224,15 +221,28 @@ __device__ __forceinline__ void conv_half(double2* X, const double2* tw, const d
   auto lds = [&](int i) { return X[phys(i)]; };
   auto sts = [&](int i, double2 v) { X[phys(i)] = v; };
   __syncthreads();
+  if (!MWSHT_FFT_FUSE_IO) {
+    // streaming fill: independent iterations keep many global loads in flight
+#pragma unroll 4
+    for (int j = threadIdx.x; j < H; j += kT) X[phys(j)] = in(j);
+    __syncthreads();
+  }
   if (np == 1) {
-    pass_r<2>(logH, tw, S, H, M, H, in, out);
+    if (MWSHT_FFT_FUSE_IO) {
+      pass_r<2>(logH, tw, S, H, M, H, in, out);
+    } else {
+      pass_r<2>(logH, tw, S, H, M, H, lds, sts);
+      __syncthreads();
+#pragma unroll 4
+      for (int k = threadIdx.x; k < H; k += kT) out(k, X[phys(k)]);
+    }
     __syncthreads();
     return;
   }
   int n = H;
   for (int p = 0; p < np - 1; p++) {
     const int lr = nlog(logH, p);
-    if (p == 0)
+    if (p == 0 && MWSHT_FFT_FUSE_IO)
       pass_r<0>(lr, tw, S, H, M, n, in, sts);
     else
       pass_r<0>(lr, tw, S, H, M, n, lds, sts);
@@ -244,10 +254,15 @@ __device__ __forceinline__ void conv_half(double2* X, const double2* tw, const d
   for (int p = np - 2; p >= 0; p--) {
     const int lr = nlog(logH, p);
     n <<= lr;
-    if (p == 0)
+    if (p == 0 && MWSHT_FFT_FUSE_IO)
       pass_r<1>(lr, tw, S, H, M, n, lds, out);
     else
       pass_r<1>(lr, tw, S, H, M, n, lds, sts);
+    __syncthreads();
+  }
+  if (!MWSHT_FFT_FUSE_IO) {
+#pragma unroll 4
+    for (int k = threadIdx.x; k < H; k += kT) out(k, X[phys(k)]);
     __syncthreads();
   }
 }
@@ -305,16 +320,16 @@ __global__ void __launch_bounds__(kT, 1) k_phi_fwd(FftArgs a) {
   const int kout = REAL ? L : N;
   const double sc = 2.0 * 3.141592653589793 / (double)N / (double)a.M;
   for (int row = blockIdx.x; row < a.nrows * a.nmaps; row += gridDim.x) {
-    const int map = row / a.nrows, t = row - map * a.nrows;
+    const int map = row / a.nrows, tl = row - map * a.nrows, t = a.t0 + tl;
     double2* at = (double2*)a.out + (long long)map * a.out_stride;
     auto fin = [&](int k, double2 y) {
       if (k < kout) at[(long long)k * L + t] = cscale(cmulc(y, a.chirp[k]), sc);
     };
     if (REAL) {
-      const double* f = (const double*)a.in + (long long)map * a.in_stride + (long long)t * N;
+      const double* f = (const double*)a.in + (long long)map * a.in_stride + (long long)tl * N;
       bluestein<false>(X, tws, scr, a, [&](int n) { return make_double2(f[n], 0.0); }, fin);
     } else {
-      const double2* f = (const double2*)a.in + (long long)map * a.in_stride + (long long)t * N;
+      const double2* f = (const double2*)a.in + (long long)map * a.in_stride + (long long)tl * N;
       bluestein<false>(X, tws, scr, a, [&](int n) { return f[n]; }, fin);
     }
   }
@@ -335,7 +350,7 @@ __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
   const int L = a.L, N = a.N, H = a.H, M = a.M, ldw = a.ldw;
   for (int row = blockIdx.x; row < a.nrows * a.nmaps; row += gridDim.x) {
     const int map = row / a.nrows, r = row - map * a.nrows;
-    const int m = REAL ? r : r - (L - 1);
+    const int m = row_order(r, a.m0, a.m1, REAL);
     const bool neg = !REAL && m < 0;
     const int am = neg ? -m : m;
     const double eps = (((m + (REAL ? 0 : a.spin)) & 1) ? -1.0 : 1.0);
@@ -395,10 +410,12 @@ __global__ void __launch_bounds__(kT, 1) k_theta_inv(FftArgs a) {
   const int ocols = REAL ? L : N;
   const double inv = 1.0 / (double)a.M;
   for (int row = blockIdx.x; row < a.nrows * a.nmaps; row += gridDim.x) {
-    const int map = row / a.nrows, r = row - map * a.nrows;
+    const int map = row / a.nrows, i = row - map * a.nrows;
+    const int m = row_order(i, a.m0, a.m1, REAL);
+    const int r = REAL ? m : m + (L - 1);  // plane row of order m
     const double2* s = (const double2*)a.in + (long long)map * a.in_stride + (long long)r * N;
     double2* o = (double2*)a.out + (long long)map * a.out_stride;
-    const int col = REAL ? r : fbin(r - (L - 1), N);
+    const int col = REAL ? m : fbin(m, N);
     bluestein<true>(X, tws, scr, a, [&](int n) { return s[n]; }, [&](int t, double2 y) {
       if (t < L) {
         double2 v = cscale(cmul(y, a.chirp[t]), inv);
@@ -421,10 +438,10 @@ __global__ void __launch_bounds__(kT, 1) k_phi_inv(FftArgs a) {
   const int L = a.L, N = a.N;
   const double inv = 1.0 / (double)a.M;
   for (int row = blockIdx.x; row < a.nrows * a.nmaps; row += gridDim.x) {
-    const int map = row / a.nrows, t = row - map * a.nrows;
+    const int map = row / a.nrows, tl = row - map * a.nrows, t = a.t0 + tl;
     if (REAL) {
       const double2* h = (const double2*)a.in + (long long)map * a.in_stride + (long long)t * L;
-      double* o = (double*)a.out + (long long)map * a.out_stride + (long long)t * N;
+      double* o = (double*)a.out + (long long)map * a.out_stride + (long long)tl * N;
       bluestein<true>(
           X, tws, scr, a, [&](int n) { return n < L ? h[n] : conjd(h[N - n]); },
           [&](int p, double2 y) {
@@ -432,7 +449,7 @@ __global__ void __launch_bounds__(kT, 1) k_phi_inv(FftArgs a) {
           });
     } else {
       const double2* h = (const double2*)a.in + (long long)map * a.in_stride + (long long)t * N;
-      double2* o = (double2*)a.out + (long long)map * a.out_stride + (long long)t * N;
+      double2* o = (double2*)a.out + (long long)map * a.out_stride + (long long)tl * N;
       bluestein<true>(X, tws, scr, a, [&](int n) { return h[n]; }, [&](int p, double2 y) {
         if (p < N) o[p] = cscale(cmul(y, a.chirp[p]), inv);
       });

@@ -33,22 +33,6 @@ void launch_untranspose(bool real, const double2* S, double2* Out, int L, int N,
                         long long os, int nm, cudaStream_t st);
 void launch_reality(const double2* f, int L, unsigned long long* worst, unsigned long long* peak,
                     cudaStream_t st);
-namespace fft {
-struct FftArgs {
-  int L, N, M, H, logH, ldw, spin;
-  const double2* tw;
-  const double2* chirp;
-  const double2* specf;
-  const double2* speci;
-  const double2* specw;
-  const double2* rho;
-  double2* scratch;
-  const void* in;
-  void* out;
-  long long in_stride, out_stride;
-  int nrows, nmaps;
-};
-}  // namespace fft
 void fft_launch(int which, bool real, const fft::FftArgs& a, int nsm, cudaStream_t st);
 void fft_spectrum(const fft::FftArgs& a, const double2* kern, double2* spec, cudaStream_t st);
 }  // namespace mwsht
@@ -91,6 +75,11 @@ struct mwsht_plan {
   std::map<int, SpinTab> spins;
   int2 *tiles_inv = nullptr, *tiles_fwd = nullptr;
   int ntiles_inv = 0, ntiles_fwd = 0;
+  struct TileSet {
+    int2 *inv = nullptr, *fwd = nullptr;
+    int ninv = 0, nfwd = 0;
+  };
+  std::map<std::pair<int, int>, TileSet> range_tiles;  // tiles with c0 in [m0, m1)
   // fused FFT engine (fft.cu): M-point FFT-convolutions in H = M/2 smem halves
   int M = 0, H = 0, logH = 0, nsm = 0;
   double2 *tw = nullptr, *chirp = nullptr, *specf = nullptr, *speci = nullptr, *specw = nullptr,
@@ -322,6 +311,44 @@ static int build_tiles(mwsht_plan* p) {
   return MWSHT_OK;
 }
 
+// Core tile lists restricted to orders m0 <= m < m1 (m-column sharding,
+// SURVEY.md §8e); same heavy-first order as build_tiles.
+static int range_tiles(mwsht_plan* p, int m0, int m1, mwsht_plan::TileSet** out) {
+  auto key = std::make_pair(m0, m1);
+  auto it = p->range_tiles.find(key);
+  if (it == p->range_tiles.end()) {
+    const int L = p->L;
+    struct Tl {
+      int2 t;
+      long long w;
+    };
+    std::vector<Tl> inv, fwd;
+    for (int r0 = 0; r0 < L; r0 += kTileRows)
+      for (int c0 = m0; c0 < m1; c0 += kTileCols)
+        inv.push_back({make_int2(r0, c0), (long long)(L - std::max(r0, c0))});
+    for (int l0 = 0; l0 < L; l0 += kTileRows) {
+      const int top = std::min(l0 + kTileRows - 1, L - 1);
+      for (int c0 = m0; c0 < m1 && c0 <= top; c0 += kTileCols)
+        fwd.push_back({make_int2(l0, c0), (long long)top + 1});
+    }
+    auto by_work = [](const Tl& a, const Tl& b) { return a.w > b.w; };
+    std::stable_sort(inv.begin(), inv.end(), by_work);
+    std::stable_sort(fwd.begin(), fwd.end(), by_work);
+    std::vector<int2> hi, hf;
+    for (auto& x : inv) hi.push_back(x.t);
+    for (auto& x : fwd) hf.push_back(x.t);
+    mwsht_plan::TileSet ts;
+    int rc;
+    if (!hi.empty() && (rc = upload(p, &ts.inv, hi))) return rc;
+    if (!hf.empty() && (rc = upload(p, &ts.fwd, hf))) return rc;
+    ts.ninv = (int)hi.size();
+    ts.nfwd = (int)hf.size();
+    it = p->range_tiles.emplace(key, ts).first;
+  }
+  *out = &it->second;
+  return MWSHT_OK;
+}
+
 // Fused-FFT tables (fft.cu): quarter twiddles w_M^j, chirp c[n] = e^{i pi n^2/N},
 // spectra (half-split DIF of the Bluestein kernels c, conj c and of the
 // weight-correlation kernel K'[d mod M] = 2 pi w(-d), |d| <= 2L-2,
@@ -343,6 +370,9 @@ static fft::FftArgs fft_args(mwsht_plan* p) {
   a.rho = p->rho;
   a.scratch = p->scratch;
   a.nmaps = 1;
+  a.m0 = 0;
+  a.m1 = p->L;
+  a.t0 = 0;
   return a;
 }
 
@@ -798,6 +828,119 @@ int mwsht_forward_stages_z(mwsht_plan* p, const void* samples, void* gfold, int 
   p->own_launches = 0;
   if ((rc = forward_stages(p, 1, samples, false, spin, (cudaStream_t)stream))) return rc;
   launch_T2_to_fold(false, p->bufG, (double2*)gfold, p->L, p->ldw, (cudaStream_t)stream);
+  LAUNCHED(p);
+  return MWSHT_OK;
+}
+
+static int check_range(mwsht_plan* p, int m0, int m1) {
+  if (m0 < 0 || m1 > p->L || m0 >= m1 || (m0 % kTileCols) || ((m1 % kTileCols) && m1 != p->L))
+    return fail(MWSHT_E_CONTRACT, "shard", "order range must be [m0, m1) with multiples of 32 (or m1 = L)");
+  return MWSHT_OK;
+}
+
+int mwsht_shard_forward_phi(mwsht_plan* p, const void* samples_rows, int t0, int t1, void* AT,
+                            void* stream) {
+  int rc;
+  if ((rc = check_plan(p))) return rc;
+  if (t0 < 0 || t1 > p->L || t0 >= t1) return fail(MWSHT_E_CONTRACT, "shard", "bad ring range");
+  std::lock_guard<std::mutex> lk(p->mu);
+  p->own_launches = 0;
+  fft::FftArgs a = fft_args(p);
+  a.nrows = t1 - t0;
+  a.t0 = t0;
+  a.in = samples_rows;
+  a.in_stride = 0;
+  a.out = AT;
+  a.out_stride = 0;
+  fft_launch(0, false, a, p->nsm, (cudaStream_t)stream);
+  LAUNCHED(p);
+  return MWSHT_OK;
+}
+
+int mwsht_shard_forward_rest(mwsht_plan* p, const void* AT, int m0, int m1, int spin, void* flm,
+                             void* stream) {
+  int rc;
+  if ((rc = check_plan(p)) || (rc = check_spin(p, spin)) || (rc = check_range(p, m0, m1))) return rc;
+  std::lock_guard<std::mutex> lk(p->mu);
+  if ((rc = build_spin(p, spin))) return rc;
+  mwsht_plan::TileSet* ts;
+  if ((rc = range_tiles(p, m0, m1, &ts))) return rc;
+  p->own_launches = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  fft::FftArgs a = fft_args(p);
+  a.spin = spin;
+  a.m0 = m0;
+  a.m1 = m1;
+  a.nrows = 2 * (m1 - m0) - (m0 == 0 ? 1 : 0);
+  a.in = AT;
+  a.in_stride = 0;
+  a.out = p->bufG;
+  a.out_stride = p->strideG;
+  fft_launch(1, false, a, p->nsm, st);
+  LAUNCHED(p);
+  FwdArgs f = fwd_args(p, spin);
+  f.tiles = ts->fwd;
+  f.out = (double2*)flm;
+  f.out_mode = 0;
+  f.out_stride = (long long)p->L * p->L;
+  if (ts->nfwd) {
+    launch_forward_core(f, ts->nfwd, 1, false, st);
+    LAUNCHED(p);
+  }
+  return MWSHT_OK;
+}
+
+int mwsht_shard_inverse_front(mwsht_plan* p, const void* flm, int m0, int m1, int spin, void* OUT,
+                              void* stream) {
+  int rc;
+  if ((rc = check_plan(p)) || (rc = check_spin(p, spin)) || (rc = check_range(p, m0, m1))) return rc;
+  std::lock_guard<std::mutex> lk(p->mu);
+  if ((rc = build_spin(p, spin))) return rc;
+  mwsht_plan::TileSet* ts;
+  if ((rc = range_tiles(p, m0, m1, &ts))) return rc;
+  p->own_launches = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int L = p->L, N = p->N;
+  launch_inv_prescale(false, (const double2*)flm, 0, p->tabs.cl, p->tabs.A, L, p->ldw, p->bufG,
+                      (long long)L * L, p->strideG, 1, st);
+  LAUNCHED(p);
+  InvArgs a = inv_args(p, spin);
+  a.tiles = ts->inv;
+  a.out = p->bufB;
+  a.out_mode = 0;
+  a.out_stride = (long long)N * N;
+  if (ts->ninv) {
+    launch_inverse_core(a, ts->ninv, 1, false, st);
+    LAUNCHED(p);
+  }
+  fft::FftArgs f = fft_args(p);
+  f.m0 = m0;
+  f.m1 = m1;
+  f.nrows = 2 * (m1 - m0) - (m0 == 0 ? 1 : 0);
+  f.in = p->bufB;
+  f.in_stride = 0;
+  f.out = OUT;
+  f.out_stride = 0;
+  fft_launch(2, false, f, p->nsm, st);
+  LAUNCHED(p);
+  return MWSHT_OK;
+}
+
+int mwsht_shard_inverse_phi(mwsht_plan* p, const void* OUT, int t0, int t1, void* samples_rows,
+                            void* stream) {
+  int rc;
+  if ((rc = check_plan(p))) return rc;
+  if (t0 < 0 || t1 > p->L || t0 >= t1) return fail(MWSHT_E_CONTRACT, "shard", "bad ring range");
+  std::lock_guard<std::mutex> lk(p->mu);
+  p->own_launches = 0;
+  fft::FftArgs f = fft_args(p);
+  f.nrows = t1 - t0;
+  f.t0 = t0;
+  f.in = OUT;
+  f.in_stride = 0;
+  f.out = samples_rows;
+  f.out_stride = 0;
+  fft_launch(3, false, f, p->nsm, (cudaStream_t)stream);
   LAUNCHED(p);
   return MWSHT_OK;
 }
