@@ -44,9 +44,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 WORKLOADS = {
-    "c5s0": dict(L=4096, spin=0, real=False, maps=1, shard="replica",
+    "c5s0": dict(L=4096, spin=0, real=False, maps=1, shard="mcolumn",
                  name="C5: L=4096 spin 0 complex128, single map"),
-    "c5s2": dict(L=4096, spin=2, real=False, maps=1, shard="replica",
+    "c5s2": dict(L=4096, spin=2, real=False, maps=1, shard="mcolumn",
                  name="C5: L=4096 spin 2 complex128, single map"),
     "c3": dict(L=1024, spin=0, real=True, maps=1, shard="replica",
                name="C3: L=1024 spin 0 real signal (forward_real/inverse_real)"),
@@ -209,7 +209,10 @@ def make_inputs(wl, rank, ws, torch, dev):
     from oracle import mw_oracle as O
     L, spin, real = wl["L"], wl["spin"], wl["real"]
     if wl["shard"] == "maps":
-        mine = [k for k in range(wl["maps"]) if k % ws == rank]
+        from paper_1110_6298_b200.shard import shard_maps
+        mine = shard_maps(wl["maps"], ws, rank)
+    elif wl["shard"] == "mcolumn":
+        mine = [0]  # one map split over all ranks by order columns and rings
     else:
         mine = [rank]
     vals = []
@@ -351,6 +354,61 @@ def run_gpu(wl, steps, warmup, rank, ws, local, want_e2e=True, want_clocks=True)
     return out
 
 
+def run_gpu_mcolumn(wl, steps, warmup, rank, ws, local):
+    """C5 over ws GPUs: one map, m-column sharded.  A step is
+    inverse (core + theta synthesis of own orders, all-to-all, phi synthesis of
+    own rings) then forward (phi DFT of own rings, all-to-all, theta stage + core
+    of own orders, all-reduce of the coefficients)."""
+    import torch
+    from paper_1110_6298_b200.shard import MColumnSharding
+    torch.cuda.set_device(local)
+    L, spin = wl["L"], wl["spin"]
+    host, _ = make_inputs(wl, rank, ws, torch, local)
+    sh = MColumnSharding(L, ws, rank, local)
+    flm = torch.from_numpy(host[0]).to(f"cuda:{local}")
+    stream = torch.cuda.current_stream(local)
+
+    def step():
+        rings = sh.inverse(flm, spin)
+        return sh.forward(rings, spin)
+
+    for _ in range(warmup):
+        out = step()
+    torch.cuda.synchronize()
+    err = float((out - flm).abs().max().item())
+    barrier(ws)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        out = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total = max_over_ranks(e0.elapsed_time(e1), ws)
+    # e2e: coefficients from pinned host memory, result back to the host, every step
+    h_in = torch.from_numpy(host[0]).pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        flm.copy_(h_in, non_blocking=True)
+        h_out.copy_(step(), non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_total = max_over_ranks(e0.elapsed_time(e1), ws)
+    return dict(total_ms=total, steps=steps, maps_per_rank=1, launches=8, inv_core_ms=0.0,
+                fwd_core_ms=0.0, fwd_stages_ms=0.0, roundtrip_err=err, clocks=clk,
+                l2="inputs larger than L2", plan_bytes=sh.plan.device_bytes(),
+                e2e_total_ms=e2e_total, h2d=host.nbytes, d2h=host.nbytes,
+                e2e_err=float(np.max(np.abs(h_out.numpy() - host[0]))),
+                splits=sh.bounds)
+
+
 def barrier(ws):
     if ws > 1:
         import torch.distributed as dist
@@ -393,7 +451,8 @@ def traffic_table():
 
 def summarize(key, wl, r, ws, peak_tf, steps, warmup, with_cpu, cpu_budget):
     L, spin, real = wl["L"], wl["spin"], wl["real"]
-    maps_total = wl["maps"] if wl["shard"] == "maps" else ws
+    maps_total = (wl["maps"] if wl["shard"] == "maps" else
+                  (1 if (wl["shard"] == "mcolumn" and ws > 1) else ws))
     pairs = maps_total * steps
     value = pairs / (r["total_ms"] / 1e3)
     w = wnz(L, spin, real)
@@ -402,6 +461,9 @@ def summarize(key, wl, r, ws, peak_tf, steps, warmup, with_cpu, cpu_budget):
     inv_tf = w * nm / (r["inv_core_ms"] / 1e3) / 1e12 if r["inv_core_ms"] > 0 else None
     dom = "forward_core" if r["fwd_core_ms"] >= r["inv_core_ms"] else "inverse_core"
     ach = fwd_tf if dom == "forward_core" else inv_tf
+    if ach is None:  # sharded run: whole-step rate per GPU (both directions' W_nz)
+        dom = "whole step, per GPU"
+        ach = 2 * w * maps_total * steps / (r["total_ms"] / 1e3) / ws / 1e12
     traffic = traffic_table().get(f"{key}:{dom}")
     line = {
         "metric": "MW fwd+inv SHT transforms/sec at L=1024 & 4096; % of FP64/HBM roofline",
@@ -412,14 +474,17 @@ def summarize(key, wl, r, ws, peak_tf, steps, warmup, with_cpu, cpu_budget):
         "warmup": warmup,
         "ms_per_step": r["total_ms"] / steps,
         "higher_is_better": True,
-        "scaling": "strong" if wl["shard"] == "maps" else "weak",
+        "scaling": "strong" if wl["shard"] in ("maps", "mcolumn") else "weak",
         "vs_baseline": None,
         "dtype": "f64 (complex128)",
         "data": "synthetic: seeded N(0,1) coefficients (PCG64), BASELINE.json configs",
         "config": {"workload": wl["name"], "L": L, "spin": spin, "real": real,
                    "maps_per_rank": nm, "maps_total": maps_total,
-                   "parallelism": (f"maps sharded over {ws} ranks" if wl["shard"] == "maps"
-                                   else f"{ws} independent replicas (one map per rank)"),
+                   "parallelism": (f"maps sharded over {ws} ranks" if wl["shard"] == "maps" else
+                                   (f"one map, m-column sharded over {ws} ranks (orders "
+                                    f"{r.get('splits')}), NCCL all-to-all transposes"
+                                    if (wl["shard"] == "mcolumn" and ws > 1) else
+                                    f"{ws} independent replicas (one map per rank)")),
                    "l2": r["l2"], "recursion": "trapani (drop-in default; same GPU recursion "
                                                "as risbo)"},
         "roofline": {"bound": "fp64", "kernel": dom, "achieved": ach, "peak": peak_tf,
@@ -500,11 +565,14 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
     peak = fp64_peak(local)
-    r = run_gpu(wl, args.steps, args.warmup, rank, ws, local)
+    if wl["shard"] == "mcolumn" and ws > 1:
+        r = run_gpu_mcolumn(wl, args.steps, args.warmup, rank, ws, local)
+    else:
+        r = run_gpu(wl, args.steps, args.warmup, rank, ws, local)
     line = summarize(args.workload, wl, r, ws, peak, args.steps, args.warmup,
                      with_cpu=(rank == 0 and ws == 1), cpu_budget=args.cpu_budget)
     line["fp64_peak_tflops_measured"] = peak
-    if not args.no_extra and args.workload == "c5s0":
+    if not args.no_extra and args.workload == "c5s0" and ws == 1:
         extra = {}
         for key in ("c3", "c5s2"):
             wk = WORKLOADS[key]

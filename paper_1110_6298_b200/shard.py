@@ -89,6 +89,8 @@ def _is_nccl(group=None):
 
 def all_to_all(send, recv_shapes, dtype, device, group=None):
     """send[q] -> rank q; returns recv[r] (shape recv_shapes[r]) from rank r."""
+    if not dist.is_initialized():
+        return [send[0].contiguous()]
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     recv = [torch.empty(shp, dtype=dtype, device=device) for shp in recv_shapes]
