@@ -141,24 +141,42 @@ __device__ __forceinline__ void powers(double2 (&w)[R], double2 w1) {
   for (int k = 2; k < R; k++) w[k] = cmul(w[k / 2], w[k - k / 2]);
 }
 
-// radix schedule: log-radices of the DIF passes (outer first), each <= 4
-__device__ __forceinline__ int npass(int logH) { return (logH + 3) / 4; }
-__device__ __forceinline__ int nlog(int logH, int p) {
-  const int np = npass(logH);
-  const int base = logH / np, extra = logH - base * np;
-  return base + (p < extra ? 1 : 0);
+// ------------------------------------------------------------ schedule
+// Compile-time plan for H = 2^LOGH: NP passes of radix <= 16 (outer first),
+// TEAM threads per row (one radix-16 butterfly each), NR rows in flight per
+// 512-thread CTA, each team with its own buffer and named barrier.
+template <int LOGH>
+struct Cfg {
+  static constexpr int H = 1 << LOGH;
+  static constexpr int M = 2 * H;
+  static constexpr int NP = (LOGH + 3) / 4;
+  static constexpr int TEAM = (H / 16) < 32 ? 32 : ((H / 16) > kT ? kT : (H / 16));
+  static constexpr int NR = kT / TEAM;
+  static constexpr int lr(int p) { return LOGH / NP + (p < LOGH - (LOGH / NP) * NP ? 1 : 0); }
+  static constexpr int n_at(int p) {  // sub-length of DIF pass p
+    int n = H;
+    for (int q = 0; q < p; q++) n >>= lr(q);
+    return n;
+  }
+};
+
+template <int TEAM>
+__device__ __forceinline__ void team_sync(int team) {
+  if (TEAM <= 32)
+    __syncwarp();
+  else
+    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(TEAM) : "memory");
 }
 
-// One radix-R pass on sub-length n (stride s = n/R).  MODE:
+// One radix-R pass on sub-length n (stride s = n/R), compile-time shape.  MODE:
 //   0 DIF   (load via LD, butterfly, twiddle, store via ST)
 //   1 DIT   (load, untwiddle, inverse butterfly, store)
 //   2 fused innermost DIF + spectrum multiply + innermost DIT (s = 1, j = 0)
-template <int R, int MODE, class LD, class ST>
-__device__ __forceinline__ void pass(const double2* tw, const double2* spec, int H, int M, int n,
-                                     LD ld, ST st) {
-  const int s = n / R, nb = H / R, tstep = M / n;
+template <int R, int MODE, int H, int M, int n, int TEAM, class LD, class ST>
+__device__ __forceinline__ void pass(const double2* tw, const double2* spec, int lt, LD ld, ST st) {
+  constexpr int s = n / R, nb = H / R, tstep = M / n;
 #pragma unroll 2
-  for (int b = threadIdx.x; b < nb; b += kT) {
+  for (int b = lt; b < nb; b += TEAM) {
     const int blk = b / s, j = b - blk * s, base = blk * n + j;
     double2 x[R];
     if (MODE == 0) {
@@ -182,7 +200,7 @@ __device__ __forceinline__ void pass(const double2* tw, const double2* spec, int
     } else {
       double2 sp[R];
 #pragma unroll
-      for (int k = 0; k < R; k++) sp[k] = spec[base + k];  // in flight during the butterfly
+      for (int k = 0; k < R; k++) sp[k] = spec[base + k];
 #pragma unroll
       for (int r = 0; r < R; r++) x[r] = ld(base + r);
       net_fwd<R>(x);
@@ -195,75 +213,55 @@ __device__ __forceinline__ void pass(const double2* tw, const double2* spec, int
   }
 }
 
-template <int MODE, class LD, class ST>
-__device__ __forceinline__ void pass_r(int lr, const double2* tw, const double2* spec, int H, int M,
-                                       int n, LD ld, ST st) {
-  switch (lr) {
-    case 1: pass<2, MODE>(tw, spec, H, M, n, ld, st); break;
-    case 2: pass<4, MODE>(tw, spec, H, M, n, ld, st); break;
-    case 3: pass<8, MODE>(tw, spec, H, M, n, ld, st); break;
-    default: pass<16, MODE>(tw, spec, H, M, n, ld, st); break;
+template <int LOGH, int P, class IN, class LDS, class STS>
+__device__ __forceinline__ void dif_chain(const double2* tw, int lt, int team, IN in, LDS lds,
+                                          STS sts) {
+  using C = Cfg<LOGH>;
+  if constexpr (P < C::NP - 1) {
+    constexpr int R = 1 << C::lr(P), n = C::n_at(P);
+    if constexpr (P == 0)
+      pass<R, 0, C::H, C::M, n, C::TEAM>(tw, nullptr, lt, in, sts);
+    else
+      pass<R, 0, C::H, C::M, n, C::TEAM>(tw, nullptr, lt, lds, sts);
+    team_sync<C::TEAM>(team);
+    dif_chain<LOGH, P + 1>(tw, lt, team, in, lds, sts);
   }
 }
 
-// z = DIT_H( DIF_H(x) . S ), x given by IN(j), z delivered to OUT(k, z_k)
-// (unnormalised).  The first DIF pass reads IN directly, the innermost DIF
-// pass, the spectrum multiply and the innermost DIT pass are one register
-// pass, and the last DIT pass hands results to OUT, so the H-point buffer X
-// is touched by 2*(np-1) shared-memory passes instead of 2*np + 2.
-#ifndef MWSHT_FFT_FUSE_IO
-#define MWSHT_FFT_FUSE_IO 0
-#endif
-template <class IN, class OUT>
-__device__ __forceinline__ void conv_half(double2* X, const double2* tw, const double2* S,
-                                          const FftArgs& a, IN in, OUT out) {
-  const int H = a.H, M = a.M, logH = a.logH, np = npass(logH);
+template <int LOGH, int P, class OUT, class LDS, class STS>
+__device__ __forceinline__ void dit_chain(const double2* tw, int lt, int team, OUT out, LDS lds,
+                                          STS sts) {
+  using C = Cfg<LOGH>;
+  if constexpr (P >= 0) {
+    constexpr int R = 1 << C::lr(P), n = C::n_at(P);
+    if constexpr (P == 0)
+      pass<R, 1, C::H, C::M, n, C::TEAM>(tw, nullptr, lt, lds, out);
+    else
+      pass<R, 1, C::H, C::M, n, C::TEAM>(tw, nullptr, lt, lds, sts);
+    team_sync<C::TEAM>(team);
+    dit_chain<LOGH, P - 1>(tw, lt, team, out, lds, sts);
+  }
+}
+
+// z = DIT_H( DIF_H(x) . S ), x from IN(j), z delivered to OUT(k, z_k) (unnormalised).
+// The first DIF pass reads IN, the innermost DIF pass + spectrum multiply +
+// innermost DIT pass are one register pass, the last DIT pass hands results to OUT.
+template <int LOGH, class IN, class OUT>
+__device__ __forceinline__ void conv_half(double2* X, const double2* tw, const double2* S, int lt,
+                                          int team, IN in, OUT out) {
+  using C = Cfg<LOGH>;
   auto lds = [&](int i) { return X[phys(i)]; };
   auto sts = [&](int i, double2 v) { X[phys(i)] = v; };
-  __syncthreads();
-  if (!MWSHT_FFT_FUSE_IO) {
-    // streaming fill: independent iterations keep many global loads in flight
-#pragma unroll 4
-    for (int j = threadIdx.x; j < H; j += kT) X[phys(j)] = in(j);
-    __syncthreads();
-  }
-  if (np == 1) {
-    if (MWSHT_FFT_FUSE_IO) {
-      pass_r<2>(logH, tw, S, H, M, H, in, out);
-    } else {
-      pass_r<2>(logH, tw, S, H, M, H, lds, sts);
-      __syncthreads();
-#pragma unroll 4
-      for (int k = threadIdx.x; k < H; k += kT) out(k, X[phys(k)]);
-    }
-    __syncthreads();
-    return;
-  }
-  int n = H;
-  for (int p = 0; p < np - 1; p++) {
-    const int lr = nlog(logH, p);
-    if (p == 0 && MWSHT_FFT_FUSE_IO)
-      pass_r<0>(lr, tw, S, H, M, n, in, sts);
-    else
-      pass_r<0>(lr, tw, S, H, M, n, lds, sts);
-    n >>= lr;
-    __syncthreads();
-  }
-  pass_r<2>(nlog(logH, np - 1), tw, S, H, M, n, lds, sts);
-  __syncthreads();
-  for (int p = np - 2; p >= 0; p--) {
-    const int lr = nlog(logH, p);
-    n <<= lr;
-    if (p == 0 && MWSHT_FFT_FUSE_IO)
-      pass_r<1>(lr, tw, S, H, M, n, lds, out);
-    else
-      pass_r<1>(lr, tw, S, H, M, n, lds, sts);
-    __syncthreads();
-  }
-  if (!MWSHT_FFT_FUSE_IO) {
-#pragma unroll 4
-    for (int k = threadIdx.x; k < H; k += kT) out(k, X[phys(k)]);
-    __syncthreads();
+  team_sync<C::TEAM>(team);
+  constexpr int RL = 1 << C::lr(C::NP - 1), nL = C::n_at(C::NP - 1);
+  if constexpr (C::NP == 1) {
+    pass<RL, 2, C::H, C::M, nL, C::TEAM>(tw, S, lt, in, out);
+    team_sync<C::TEAM>(team);
+  } else {
+    dif_chain<LOGH, 0>(tw, lt, team, in, lds, sts);
+    pass<RL, 2, C::H, C::M, nL, C::TEAM>(tw, S, lt, lds, sts);
+    team_sync<C::TEAM>(team);
+    dit_chain<LOGH, C::NP - 2>(tw, lt, team, out, lds, sts);
   }
 }
 
@@ -277,17 +275,18 @@ __device__ __forceinline__ int fbin(int k, int N) { return k >= 0 ? k : k + N; }
 // Bluestein DFT_N of x (fx(n), n < N): forward (conj chirp, spec f) or inverse
 // (chirp, spec i).  Half 1 leaves z1 in scr; half 0 calls fin(k, y_k) with the
 // merged y[k] = z0[k] + w^-k z1[k] (unnormalised; DFT = chirp' . y / M).
-template <bool INV, class FX, class FIN>
+template <int LOGH, bool INV, class FX, class FIN>
 __device__ __forceinline__ void bluestein(double2* X, const double2* tw, double2* scr,
-                                          const FftArgs& a, FX fx, FIN fin) {
+                                          const FftArgs& a, int lt, int team, FX fx, FIN fin) {
+  using C = Cfg<LOGH>;
   const double2* spec = INV ? a.speci : a.specf;
-  const int N = a.N, M = a.M;
+  const int N = a.N;
   auto in1 = [&](int j) {
     double2 v = make_double2(0.0, 0.0);
     if (j < N) {
       const double2 c = a.chirp[j];
       v = INV ? cmul(fx(j), c) : cmulc(fx(j), c);
-      v = cmul(v, omega(tw, j, M));
+      v = cmul(v, omega(tw, j, C::M));
     }
     return v;
   };
@@ -300,26 +299,32 @@ __device__ __forceinline__ void bluestein(double2* X, const double2* tw, double2
     return v;
   };
   auto out1 = [&](int k, double2 v) { scr[k] = v; };
-  auto out0 = [&](int k, double2 v) { fin(k, cadd(v, cmulc(scr[k], omega(tw, k, M)))); };
-  conv_half(X, tw, spec + a.H, a, in1, out1);
-  conv_half(X, tw, spec, a, in0, out0);
+  auto out0 = [&](int k, double2 v) { fin(k, cadd(v, cmulc(scr[k], omega(tw, k, C::M)))); };
+  conv_half<LOGH>(X, tw, spec + C::H, lt, team, in1, out1);
+  conv_half<LOGH>(X, tw, spec, lt, team, in0, out0);
 }
+
+// Per-CTA setup shared by the stage kernels: team split, buffers, twiddles.
+#define FFT_PROLOGUE                                                         \
+  using C = Cfg<LOGH>;                                                       \
+  extern __shared__ __align__(16) double2 sm[];                              \
+  const int team = threadIdx.x / C::TEAM, lt = threadIdx.x - team * C::TEAM; \
+  double2* X = sm + team * C::H;                                             \
+  double2* tws = sm + C::NR * C::H;                                          \
+  load_tw(tws, a);                                                           \
+  double2* scr = a.scratch + ((long long)blockIdx.x * C::NR + team) * 2 * C::H;
 
 // ------------------------------------------------------------------ kernels
 
 // phi DFT of each ring (forward): AT[k][t] = (2 pi/N) sum_p f[t][p] e^{-2 pi i kp/N}
 // complex: k < N, AT is (N, L); real: k < L (rfft bins), AT is (L, L).
-template <bool REAL>
+template <bool REAL, int LOGH>
 __global__ void __launch_bounds__(kT, 1) k_phi_fwd(FftArgs a) {
-  extern __shared__ __align__(16) double2 sm[];
-  double2* X = sm;
-  double2* tws = sm + a.H;
-  load_tw(tws, a);
-  double2* scr = a.scratch + (long long)blockIdx.x * 2 * a.H;
+  FFT_PROLOGUE
   const int L = a.L, N = a.N;
   const int kout = REAL ? L : N;
-  const double sc = 2.0 * 3.141592653589793 / (double)N / (double)a.M;
-  for (int row = blockIdx.x; row < a.nrows * a.nmaps; row += gridDim.x) {
+  const double sc = 2.0 * 3.141592653589793 / (double)N / (double)C::M;
+  for (int row = blockIdx.x * C::NR + team; row < a.nrows * a.nmaps; row += gridDim.x * C::NR) {
     const int map = row / a.nrows, tl = row - map * a.nrows, t = a.t0 + tl;
     double2* at = (double2*)a.out + (long long)map * a.out_stride;
     auto fin = [&](int k, double2 y) {
@@ -327,28 +332,26 @@ __global__ void __launch_bounds__(kT, 1) k_phi_fwd(FftArgs a) {
     };
     if (REAL) {
       const double* f = (const double*)a.in + (long long)map * a.in_stride + (long long)tl * N;
-      bluestein<false>(X, tws, scr, a, [&](int n) { return make_double2(f[n], 0.0); }, fin);
+      bluestein<LOGH, false>(X, tws, scr, a, lt, team,
+                             [&](int n) { return make_double2(f[n], 0.0); }, fin);
     } else {
       const double2* f = (const double2*)a.in + (long long)map * a.in_stride + (long long)tl * N;
-      bluestein<false>(X, tws, scr, a, [&](int n) { return f[n]; }, fin);
+      bluestein<LOGH, false>(X, tws, scr, a, lt, team, [&](int n) { return f[n]; }, fin);
     }
   }
 }
 
-// theta stage of the forward transform for each order row r (complex: r < N,
-// m = r-(L-1); real: r < L, m = r): extension (mw.py:161-177), DFT_N + twist
-// (:180-192), weight correlation (:244-251) and m' fold (:273-285, 504-511),
-// written in the forward core's staging layout gfT (ldw columns, +m / -m halves).
-template <bool REAL>
+// theta stage of the forward transform for each order row (m from row_order):
+// extension (mw.py:161-177), DFT_N + twist (:180-192), weight correlation
+// (:244-251) and m' fold (:273-285, 504-511), written in the forward core's
+// staging layout gfT (ldw columns, +m / -m halves).
+template <bool REAL, int LOGH>
 __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
-  extern __shared__ __align__(16) double2 sm[];
-  double2* X = sm;
-  double2* tws = sm + a.H;
-  load_tw(tws, a);
-  double2* scr = a.scratch + (long long)blockIdx.x * 2 * a.H;  // z1
-  double2* scrF = scr + a.H;                                     // F_raw (N)
-  const int L = a.L, N = a.N, H = a.H, M = a.M, ldw = a.ldw;
-  for (int row = blockIdx.x; row < a.nrows * a.nmaps; row += gridDim.x) {
+  FFT_PROLOGUE
+  double2* scrF = scr + C::H;  // F_raw (N <= H)
+  const int L = a.L, N = a.N, ldw = a.ldw;
+  constexpr int H = C::H, M = C::M;
+  for (int row = blockIdx.x * C::NR + team; row < a.nrows * a.nmaps; row += gridDim.x * C::NR) {
     const int map = row / a.nrows, r = row - map * a.nrows;
     const int m = row_order(r, a.m0, a.m1, REAL);
     const bool neg = !REAL && m < 0;
@@ -357,31 +360,32 @@ __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
     const double2* g = (const double2*)a.in + (long long)map * a.in_stride +
                        (long long)(REAL ? m : fbin(m, N)) * L;
     // 1. Bluestein DFT_N of the periodic extension; F_raw[k] = y[k] conj(c[k]) tau(f(k))/M
-    bluestein<false>(
-        X, tws, scr, a, [&](int n) { return n < L ? g[n] : cscale(g[2 * L - 2 - n], eps); },
+    bluestein<LOGH, false>(
+        X, tws, scr, a, lt, team,
+        [&](int n) { return n < L ? g[n] : cscale(g[2 * L - 2 - n], eps); },
         [&](int k, double2 y) {
           if (k < N) scrF[k] = cmul(y, a.rho[k]);
         });
-    __syncthreads();
+    team_sync<C::TEAM>(team);
     // 2. weight correlation on F placed in FFT order (f at f mod M)
     auto Fpl = [&](int p) -> double2 {
       if (p < L) return scrF[p];
       if (p >= M - L + 1) return scrF[p - M + N];
       return make_double2(0.0, 0.0);
     };
-    conv_half(
-        X, tws, a.specw + H, a,
+    conv_half<LOGH>(
+        X, tws, a.specw + H, lt, team,
         [&](int j) { return cmul(csub(Fpl(j), Fpl(j + H)), omega(tws, j, M)); },
         [&](int k, double2 v) { scr[k] = v; });
-    conv_half(
-        X, tws, a.specw, a, [&](int j) { return cadd(Fpl(j), Fpl(j + H)); },
+    conv_half<LOGH>(
+        X, tws, a.specw, lt, team, [&](int j) { return cadd(Fpl(j), Fpl(j + H)); },
         [&](int k, double2 v) { X[phys(k)] = v; });
-    __syncthreads();
+    team_sync<C::TEAM>(team);
     // 3. G(m') = y[m' mod M]/M; fold gf[j] = G(j) + s G(-j); write staging column
     const double sig = eps;  // (-1)^(m+s) (complex) / (-1)^m (real), mw.py:273-285
     const double inv = 1.0 / (double)M;
     double2* gT = (double2*)a.out + (long long)map * a.out_stride + (neg ? (long long)L * ldw : 0);
-    for (int j = threadIdx.x; j < L; j += kT) {
+    for (int j = lt; j < L; j += C::TEAM) {
       double2 v = cadd(X[phys(j)], cmulc(scr[j], omega(tws, j, M)));
       if (j > 0) {
         const int k = H - j;  // position M - j = k + H
@@ -394,137 +398,170 @@ __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
       if (!REAL && m == 0)
         gT[(long long)L * ldw + (long long)j * ldw] = (j & 1) ? make_double2(-v.x, -v.y) : v;
     }
+    team_sync<C::TEAM>(team);
   }
 }
 
 // inverse theta synthesis per order row: rows[t] = sum_m' S[bin(m')] e^{+2 pi i m' t/N}
 // (S already carries the core's twist), keep t < L, write Out[t][col].
-template <bool REAL>
+template <bool REAL, int LOGH>
 __global__ void __launch_bounds__(kT, 1) k_theta_inv(FftArgs a) {
-  extern __shared__ __align__(16) double2 sm[];
-  double2* X = sm;
-  double2* tws = sm + a.H;
-  load_tw(tws, a);
-  double2* scr = a.scratch + (long long)blockIdx.x * 2 * a.H;
+  FFT_PROLOGUE
   const int L = a.L, N = a.N;
   const int ocols = REAL ? L : N;
-  const double inv = 1.0 / (double)a.M;
-  for (int row = blockIdx.x; row < a.nrows * a.nmaps; row += gridDim.x) {
+  const double inv = 1.0 / (double)C::M;
+  for (int row = blockIdx.x * C::NR + team; row < a.nrows * a.nmaps; row += gridDim.x * C::NR) {
     const int map = row / a.nrows, i = row - map * a.nrows;
     const int m = row_order(i, a.m0, a.m1, REAL);
     const int r = REAL ? m : m + (L - 1);  // plane row of order m
     const double2* s = (const double2*)a.in + (long long)map * a.in_stride + (long long)r * N;
     double2* o = (double2*)a.out + (long long)map * a.out_stride;
     const int col = REAL ? m : fbin(m, N);
-    bluestein<true>(X, tws, scr, a, [&](int n) { return s[n]; }, [&](int t, double2 y) {
-      if (t < L) {
-        double2 v = cscale(cmul(y, a.chirp[t]), inv);
-        if (REAL && r == 0) v.y = 0.0;  // irfft ignores Im of the DC bin
-        o[(long long)t * ocols + col] = v;
-      }
-    });
+    bluestein<LOGH, true>(X, tws, scr, a, lt, team, [&](int n) { return s[n]; },
+                          [&](int t, double2 y) {
+                            if (t < L) {
+                              double2 v = cscale(cmul(y, a.chirp[t]), inv);
+                              if (REAL && m == 0) v.y = 0.0;  // irfft ignores Im of the DC bin
+                              o[(long long)t * ocols + col] = v;
+                            }
+                          });
   }
 }
 
 // inverse phi synthesis per ring t: samples[t][p] = sum_m Out[t][bin(m)] e^{+2 pi i m p/N}
 // (real: Hermitian completion of the m >= 0 half, real part out; mw.py:558).
-template <bool REAL>
+template <bool REAL, int LOGH>
 __global__ void __launch_bounds__(kT, 1) k_phi_inv(FftArgs a) {
-  extern __shared__ __align__(16) double2 sm[];
-  double2* X = sm;
-  double2* tws = sm + a.H;
-  load_tw(tws, a);
-  double2* scr = a.scratch + (long long)blockIdx.x * 2 * a.H;
+  FFT_PROLOGUE
   const int L = a.L, N = a.N;
-  const double inv = 1.0 / (double)a.M;
-  for (int row = blockIdx.x; row < a.nrows * a.nmaps; row += gridDim.x) {
+  const double inv = 1.0 / (double)C::M;
+  for (int row = blockIdx.x * C::NR + team; row < a.nrows * a.nmaps; row += gridDim.x * C::NR) {
     const int map = row / a.nrows, tl = row - map * a.nrows, t = a.t0 + tl;
     if (REAL) {
       const double2* h = (const double2*)a.in + (long long)map * a.in_stride + (long long)t * L;
       double* o = (double*)a.out + (long long)map * a.out_stride + (long long)tl * N;
-      bluestein<true>(
-          X, tws, scr, a, [&](int n) { return n < L ? h[n] : conjd(h[N - n]); },
+      bluestein<LOGH, true>(
+          X, tws, scr, a, lt, team, [&](int n) { return n < L ? h[n] : conjd(h[N - n]); },
           [&](int p, double2 y) {
             if (p < N) o[p] = cmul(y, a.chirp[p]).x * inv;
           });
     } else {
       const double2* h = (const double2*)a.in + (long long)map * a.in_stride + (long long)t * N;
       double2* o = (double2*)a.out + (long long)map * a.out_stride + (long long)tl * N;
-      bluestein<true>(X, tws, scr, a, [&](int n) { return h[n]; }, [&](int p, double2 y) {
-        if (p < N) o[p] = cscale(cmul(y, a.chirp[p]), inv);
-      });
+      bluestein<LOGH, true>(X, tws, scr, a, lt, team, [&](int n) { return h[n]; },
+                            [&](int p, double2 y) {
+                              if (p < N) o[p] = cscale(cmul(y, a.chirp[p]), inv);
+                            });
     }
   }
 }
 
 // plan time: S_0 = DIF_H(k[j] + k[j+H]), S_1 = DIF_H((k[j] - k[j+H]) w^j) of a
-// natural-order length-M kernel k, in the digit-reversed layout conv_half uses.
-__global__ void __launch_bounds__(kT, 1) k_spectrum(FftArgs a, const double2* kern, double2* spec) {
-  extern __shared__ __align__(16) double2 sm[];
-  double2* X = sm;
-  double2* tws = sm + a.H;
-  load_tw(tws, a);
-  const int H = a.H, M = a.M, logH = a.logH, np = npass(logH);
-  auto lds = [&](int i) { return X[phys(i)]; };
-  auto sts = [&](int i, double2 v) { X[phys(i)] = v; };
-  for (int half = 0; half < 2; half++) {
-    for (int j = threadIdx.x; j < H; j += kT) {
-      const double2 u = kern[j], v = kern[j + H];
-      X[phys(j)] = half ? cmul(csub(u, v), omega(tws, j, M)) : cadd(u, v);
-    }
-    __syncthreads();
-    int n = H;
-    for (int p = 0; p < np; p++) {
-      const int lr = nlog(logH, p);
-      pass_r<0>(lr, tws, nullptr, H, M, n, lds, sts);
-      n >>= lr;
-      __syncthreads();
-    }
-    for (int j = threadIdx.x; j < H; j += kT) spec[half * H + j] = X[phys(j)];
-    __syncthreads();
+// natural-order length-M kernel k, in the digit-reversed layout conv_half uses
+// (every DIF pass including the innermost one, no spectrum).  One team.
+template <int LOGH, int P, class LDS, class STS>
+__device__ __forceinline__ void dif_all(const double2* tw, int lt, LDS lds, STS sts) {
+  using C = Cfg<LOGH>;
+  if constexpr (P < C::NP) {
+    constexpr int R = 1 << C::lr(P), n = C::n_at(P);
+    pass<R, 0, C::H, C::M, n, C::TEAM>(tw, nullptr, lt, lds, sts);
+    team_sync<C::TEAM>(0);
+    dif_all<LOGH, P + 1>(tw, lt, lds, sts);
   }
 }
 
-size_t smem_bytes(int H, int M) { return sizeof(double2) * ((size_t)H + M / 4 + 1); }
-
-template <class K>
-static void launch_persistent(K kern, const FftArgs& a, int nsm, cudaStream_t st) {
-  const size_t sm = smem_bytes(a.H, a.M);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  int grid = a.nrows * a.nmaps;
-  if (grid > nsm) grid = nsm;
-  kern<<<grid, kT, sm, st>>>(a);
+template <int LOGH>
+__global__ void __launch_bounds__(kT, 1) k_spectrum(FftArgs a, const double2* kern, double2* spec) {
+  FFT_PROLOGUE
+  (void)scr;
+  if (team != 0) return;
+  auto lds = [&](int i) { return X[phys(i)]; };
+  auto sts = [&](int i, double2 v) { X[phys(i)] = v; };
+  for (int half = 0; half < 2; half++) {
+    for (int j = lt; j < C::H; j += C::TEAM) {
+      const double2 u = kern[j], v = kern[j + C::H];
+      X[phys(j)] = half ? cmul(csub(u, v), omega(tws, j, C::M)) : cadd(u, v);
+    }
+    team_sync<C::TEAM>(0);
+    dif_all<LOGH, 0>(tws, lt, lds, sts);
+    for (int j = lt; j < C::H; j += C::TEAM) spec[half * C::H + j] = X[phys(j)];
+    team_sync<C::TEAM>(0);
+  }
 }
+
+template <int LOGH>
+size_t smem_bytes_t() {
+  using C = Cfg<LOGH>;
+  return sizeof(double2) * ((size_t)C::NR * C::H + C::M / 4 + 1);
+}
+
+template <int LOGH, class K>
+static void launch_t(K kern, const FftArgs& a, int nsm, cudaStream_t st) {
+  using C = Cfg<LOGH>;
+  const size_t sm = smem_bytes_t<LOGH>();
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  long long rows = (long long)a.nrows * a.nmaps;
+  long long grid = (rows + C::NR - 1) / C::NR;
+  if (grid > nsm) grid = nsm;
+  if (grid < 1) grid = 1;
+  kern<<<(int)grid, kT, sm, st>>>(a);
+}
+
+template <int LOGH>
+static void launch_stage(int which, bool real, const FftArgs& a, int nsm, cudaStream_t st) {
+  switch (which) {
+    case 0:
+      real ? launch_t<LOGH>(k_phi_fwd<true, LOGH>, a, nsm, st)
+           : launch_t<LOGH>(k_phi_fwd<false, LOGH>, a, nsm, st);
+      break;
+    case 1:
+      real ? launch_t<LOGH>(k_theta_fwd<true, LOGH>, a, nsm, st)
+           : launch_t<LOGH>(k_theta_fwd<false, LOGH>, a, nsm, st);
+      break;
+    case 2:
+      real ? launch_t<LOGH>(k_theta_inv<true, LOGH>, a, nsm, st)
+           : launch_t<LOGH>(k_theta_inv<false, LOGH>, a, nsm, st);
+      break;
+    default:
+      real ? launch_t<LOGH>(k_phi_inv<true, LOGH>, a, nsm, st)
+           : launch_t<LOGH>(k_phi_inv<false, LOGH>, a, nsm, st);
+      break;
+  }
+}
+
+template <int LOGH>
+static void spectrum_t(const FftArgs& a, const double2* kern, double2* spec, cudaStream_t st) {
+  const size_t sm = smem_bytes_t<LOGH>();
+  cudaFuncSetAttribute(k_spectrum<LOGH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_spectrum<LOGH><<<1, kT, sm, st>>>(a, kern, spec);
+}
+
+#define MWSHT_FFT_SIZES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13)
 
 }  // namespace fft
 
 using fft::FftArgs;
 
 void fft_launch(int which, bool real, const FftArgs& a, int nsm, cudaStream_t st) {
-  switch (which) {
-    case 0:
-      real ? fft::launch_persistent(fft::k_phi_fwd<true>, a, nsm, st)
-           : fft::launch_persistent(fft::k_phi_fwd<false>, a, nsm, st);
-      break;
-    case 1:
-      real ? fft::launch_persistent(fft::k_theta_fwd<true>, a, nsm, st)
-           : fft::launch_persistent(fft::k_theta_fwd<false>, a, nsm, st);
-      break;
-    case 2:
-      real ? fft::launch_persistent(fft::k_theta_inv<true>, a, nsm, st)
-           : fft::launch_persistent(fft::k_theta_inv<false>, a, nsm, st);
-      break;
-    default:
-      real ? fft::launch_persistent(fft::k_phi_inv<true>, a, nsm, st)
-           : fft::launch_persistent(fft::k_phi_inv<false>, a, nsm, st);
-      break;
+  switch (a.logH) {
+#define CASE(k) \
+  case k:       \
+    fft::launch_stage<k>(which, real, a, nsm, st); \
+    break;
+    MWSHT_FFT_SIZES(CASE)
+#undef CASE
   }
 }
 
 void fft_spectrum(const FftArgs& a, const double2* kern, double2* spec, cudaStream_t st) {
-  const size_t sm = fft::smem_bytes(a.H, a.M);
-  cudaFuncSetAttribute(fft::k_spectrum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  fft::k_spectrum<<<1, fft::kT, sm, st>>>(a, kern, spec);
+  switch (a.logH) {
+#define CASE(k) \
+  case k:       \
+    fft::spectrum_t<k>(a, kern, spec, st); \
+    break;
+    MWSHT_FFT_SIZES(CASE)
+#undef CASE
+  }
 }
 
 }  // namespace mwsht

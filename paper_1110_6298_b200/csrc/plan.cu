@@ -447,7 +447,8 @@ static int build_fft_tables(mwsht_plan* p) {
   int dev;
   CU(cudaGetDevice(&dev));
   CU(cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, dev));
-  if ((rc = dev_alloc(p, (void**)&p->scratch, sizeof(double2) * 2 * (size_t)p->H * p->nsm)))
+  // per CTA: NR teams x 2H complex, NR*H <= 8192 for every size (fft.cu Cfg)
+  if ((rc = dev_alloc(p, (void**)&p->scratch, sizeof(double2) * 16384 * (size_t)p->nsm)))
     return rc;
   return MWSHT_OK;
 }

@@ -19,22 +19,31 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--L", type=int, default=4096)
 ap.add_argument("--spin", type=int, default=0)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--real", action="store_true")
 a = ap.parse_args()
 L, s = a.L, a.spin
 lib = _lib.load()
 plan = mw.get_plan(L, 0)
 lib.mwsht_plan_set_timing(plan.handle, 1)
-f = torch.from_numpy(gaussian_coeffs(L, s, 0)).cuda()
-sig = torch.empty((L, 2 * L - 1), dtype=torch.complex128, device="cuda")
+from oracle.mw_oracle import gaussian_real_coeffs  # noqa: E402
+f = torch.from_numpy(gaussian_real_coeffs(L, 0) if a.real else gaussian_coeffs(L, s, 0)).cuda()
+sig = torch.empty((L, 2 * L - 1), dtype=torch.float64 if a.real else torch.complex128,
+                  device="cuda")
 back = torch.empty_like(f)
 st = _lib._P(torch.cuda.current_stream().cuda_stream)
 e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 rows = []
 for r in range(a.reps + 1):
     e[0].record()
-    _lib.check(lib.mwsht_inverse_z(plan.handle, f.data_ptr(), sig.data_ptr(), s, 0, st))
+    if a.real:
+        _lib.check(lib.mwsht_inverse_real_d(plan.handle, f.data_ptr(), sig.data_ptr(), 0, st))
+    else:
+        _lib.check(lib.mwsht_inverse_z(plan.handle, f.data_ptr(), sig.data_ptr(), s, 0, st))
     e[1].record()
-    _lib.check(lib.mwsht_forward_z(plan.handle, sig.data_ptr(), back.data_ptr(), s, 0, st))
+    if a.real:
+        _lib.check(lib.mwsht_forward_real_d(plan.handle, sig.data_ptr(), back.data_ptr(), 0, st))
+    else:
+        _lib.check(lib.mwsht_forward_z(plan.handle, sig.data_ptr(), back.data_ptr(), s, 0, st))
     e[2].record()
     torch.cuda.synchronize()
     c, g = _lib.ctypes.c_float(), _lib.ctypes.c_float()
