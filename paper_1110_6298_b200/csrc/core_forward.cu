@@ -35,6 +35,20 @@ struct Smem {
 };
 }  // namespace fwd
 
+// one level step down (x 2^-768) for every chain whose stored value reached 2^200
+template <int NE>
+__device__ __forceinline__ void rescale(double (&y)[NE], double (&y1)[NE], unsigned& lv) {
+#pragma unroll
+  for (int e = 0; e < NE; e++) {
+    if (((lv >> (4 * e)) & 15u) && above_top(y[e])) {
+      const double sh = pow2i(-kLevShift);
+      y[e] *= sh;
+      y1[e] *= sh;
+      lv -= 1u << (4 * e);
+    }
+  }
+}
+
 template <bool REAL, bool SPIN0>
 __global__ void __launch_bounds__(kCoreThreads, 1) k_forward_core(FwdArgs a) {
   constexpr int NI = 4, NJ = 2, NE = NI * NJ;
@@ -212,7 +226,8 @@ __global__ void __launch_bounds__(kCoreThreads, 1) k_forward_core(FwdArgs a) {
 #pragma unroll 2
           for (int s = 0; s < ns; s++) full_step(s);
         }
-      } else {
+      } else if (mc >= wl_min) {
+        // ---------------------------- ramp: chains starting, levels, masking
         for (int s = 0; s < ns; s++) {
           const int mu = mc - s;
           double2 qp[NI], g[NJ][NG];
@@ -259,17 +274,50 @@ __global__ void __launch_bounds__(kCoreThreads, 1) k_forward_core(FwdArgs a) {
               y1[e] = y[e];
               y[e] = yn;
             }
-          if (lv && (s & 3) == 3) {
+          if (lv && (s & 3) == 3) rescale(y, y1, lv);
+        }
+      } else {
+        // all chains started; some still carry exponent levels (masking per
+        // chunk is lossless: a chain reaching level 0 is still below 2^-568)
+        unsigned live = 0;
 #pragma unroll
-            for (int e = 0; e < NE; e++) {
-              if (((lv >> (4 * e)) & 15u) && above_top(y[e])) {
-                const double sh = pow2i(-kLevShift);
-                y[e] *= sh;
-                y1[e] *= sh;
-                lv -= 1u << (4 * e);
-              }
+        for (int e = 0; e < NE; e++) live |= (((lv >> (4 * e)) & 15u) == 0) ? (1u << e) : 0u;
+        const bool anylive = __any_sync(0xffffffffu, live != 0);
+        for (int s = 0; s < ns; s++) {
+          const int mu = mc - s;
+          double2 qp[NI];
+#pragma unroll
+          for (int i = 0; i < NI; i++) qp[i] = S.q[s][rl[i]];
+          if (anylive && (!SPIN0 || ((mu & 1) == par))) {
+            double2 g[NJ][NG];
+#pragma unroll
+            for (int j = 0; j < NJ; j++) {
+              g[j][0] = S.gp[s][cl[j]];
+              if (!REAL) g[j][NG - 1] = S.gn[s][cl[j]];
             }
+#pragma unroll
+            for (int i = 0; i < NI; i++)
+#pragma unroll
+              for (int j = 0; j < NJ; j++) {
+                const int e = i * NJ + j;
+                const double t = ((live >> e) & 1u) ? y[e] * qp[i].y : 0.0;
+#pragma unroll
+                for (int k2 = 0; k2 < NG; k2++) {
+                  acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
+                  acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
+                }
+              }
           }
+#pragma unroll
+          for (int i = 0; i < NI; i++)
+#pragma unroll
+            for (int j = 0; j < NJ; j++) {
+              const int e = i * NJ + j;
+              const double yn = fma(md[j] * qp[i].x, y[e], -y1[e]);
+              y1[e] = y[e];
+              y[e] = yn;
+            }
+          if ((s & 3) == 3) rescale(y, y1, lv);
         }
       }
     }

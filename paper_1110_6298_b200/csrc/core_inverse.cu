@@ -35,6 +35,20 @@ struct Smem {
 };
 }  // namespace inv
 
+// one level step down (x 2^-768) for every chain whose stored value reached 2^200
+template <int NE>
+__device__ __forceinline__ void rescale(double (&z)[NE], double (&zp)[NE], unsigned& lv) {
+#pragma unroll
+  for (int e = 0; e < NE; e++) {
+    if (((lv >> (4 * e)) & 15u) && above_top(z[e])) {
+      const double sh = pow2i(-kLevShift);
+      z[e] *= sh;
+      zp[e] *= sh;
+      lv -= 1u << (4 * e);
+    }
+  }
+}
+
 template <bool REAL, bool SPIN0>
 __global__ void __launch_bounds__(kCoreThreads, 1) k_inverse_core(InvArgs a) {
   constexpr int NI = 4, NJ = 2, NE = NI * NJ;
@@ -224,7 +238,7 @@ __global__ void __launch_bounds__(kCoreThreads, 1) k_inverse_core(InvArgs a) {
 #pragma unroll 2
           for (int s = 0; s < ns; s++) full_step(s);
         }
-      } else {
+      } else if (wl0_max >= lc) {
         // --------------------------------- ramp: seed injection, levels, masking
         for (int s = 0; s < ns; s++) {
           const int l = lc + s;
@@ -282,18 +296,55 @@ __global__ void __launch_bounds__(kCoreThreads, 1) k_inverse_core(InvArgs a) {
               zp[e] = z[e];
               z[e] = zn;
             }
-          if (lv && (s & 3) == 3) {
-            // growth per degree is < 4x, so a check every 4 degrees stays far below overflow
+          if (lv && (s & 3) == 3) rescale(z, zp, lv);
+        }
+      } else {
+        // all chains started; some still carry exponent levels.  A chain that
+        // reaches level 0 inside this chunk is still below 2^-568 (its true
+        // value grows at most 4x per degree), so contributions start at the
+        // next chunk without loss; masking is per chunk, not per step.
+        unsigned live = 0;  // bit e: chain e at true scale for the whole chunk
 #pragma unroll
-            for (int e = 0; e < NE; e++) {
-              if (((lv >> (4 * e)) & 15u) && above_top(z[e])) {
-                const double sh = pow2i(-kLevShift);
-                z[e] *= sh;
-                zp[e] *= sh;
-                lv -= 1u << (4 * e);
-              }
+        for (int e = 0; e < NE; e++) live |= (((lv >> (4 * e)) & 15u) == 0) ? (1u << e) : 0u;
+        const bool anylive = __any_sync(0xffffffffu, live != 0);
+        for (int s = 0; s < ns; s++) {
+          const int l = lc + s;
+          double2 rp[NI];
+          double cc[NJ];
+#pragma unroll
+          for (int i = 0; i < NI; i++) rp[i] = S.row[s][rl[i]];
+#pragma unroll
+          for (int j = 0; j < NJ; j++) cc[j] = S.colc[s][cl[j]];
+          if (anylive && (!SPIN0 || ((l & 1) == par))) {
+            double2 g[NJ][NG];
+#pragma unroll
+            for (int j = 0; j < NJ; j++) {
+              g[j][0] = S.gp[s][cl[j]];
+              if (!REAL) g[j][NG - 1] = S.gn[s][cl[j]];
             }
+#pragma unroll
+            for (int i = 0; i < NI; i++)
+#pragma unroll
+              for (int j = 0; j < NJ; j++) {
+                const int e = i * NJ + j;
+                const double t = ((live >> e) & 1u) ? z[e] * rp[i].y : 0.0;
+#pragma unroll
+                for (int k2 = 0; k2 < NG; k2++) {
+                  acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
+                  acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
+                }
+              }
           }
+#pragma unroll
+          for (int i = 0; i < NI; i++)
+#pragma unroll
+            for (int j = 0; j < NJ; j++) {
+              const int e = i * NJ + j;
+              const double zn = fma(rp[i].x * cc[j], z[e], -zp[e]);
+              zp[e] = z[e];
+              z[e] = zn;
+            }
+          if ((s & 3) == 3) rescale(z, zp, lv);
         }
       }
     }
