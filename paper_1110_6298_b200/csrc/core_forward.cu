@@ -49,8 +49,16 @@ __device__ __forceinline__ void rescale(double (&y)[NE], double (&y1)[NE], unsig
   }
 }
 
+// Spin 0 keeps the 288-thread layout (one producer warp, 168-register cap);
+// spin != 0 runs the warp-specialised 384-thread layout (see common.cuh),
+// which measured faster for it (13.7 -> 13.3 ms at L=4096) and slower for
+// spin 0 (10.4 -> 11.4 ms).
+template <bool SPIN0>
+constexpr int fwd_threads() { return SPIN0 ? kCoreThreads : kCoreThreadsWS; }
+
 template <bool REAL, bool SPIN0>
-__global__ void __launch_bounds__(kCoreThreads, 1) k_forward_core(FwdArgs a) {
+__global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArgs a) {
+  constexpr bool WS = !SPIN0;
   constexpr int NI = 4, NJ = 2, NE = NI * NJ;
   constexpr int NG = REAL ? 1 : 2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -62,9 +70,9 @@ __global__ void __launch_bounds__(kCoreThreads, 1) k_forward_core(FwdArgs a) {
   const int l0b = tile.x, c0 = tile.y;
   const int mu_top = min(l0b + kTileRows - 1, L - 1);
   const int nchunks = (mu_top + kChunk) / kChunk;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int lane = threadIdx.x & 31, wall = threadIdx.x >> 5;
 
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     for (int b = 0; b < fwd::NB; b++) {
       mbar_init(&sm.full[b], 1);
       mbar_init(&sm.empty[b], kConsumerWarps);
@@ -73,7 +81,11 @@ __global__ void __launch_bounds__(kCoreThreads, 1) k_forward_core(FwdArgs a) {
   }
   __syncthreads();
 
-  if (w == kConsumerWarps) {
+  if (WS ? wall < 4 : wall == kConsumerWarps) {
+    if (WS) {
+      setmaxnreg_dec<kProducerRegs>();
+      if (wall != 0) return;
+    }
     // ------------------------------------------------------------ producer
     const double2* gp = a.gf + (long long)blockIdx.y * a.in_stride;
     const double2* gn = gp + (long long)L * Lp;
@@ -103,6 +115,8 @@ __global__ void __launch_bounds__(kCoreThreads, 1) k_forward_core(FwdArgs a) {
   }
 
   // -------------------------------------------------------------- consumers
+  if (WS) setmaxnreg_inc<kConsumerRegs>();
+  const int w = WS ? wall - 4 : wall, tid = WS ? threadIdx.x - 128 : threadIdx.x;
   double2* __restrict__ out = a.out + (long long)blockIdx.y * a.out_stride;
   const int wr = w & 3, wc = w >> 2, r = lane & 3, c = lane >> 2, par = wr & 1;
   int rl[NI], cl[NJ], ll[NI], mm[NJ];
@@ -378,7 +392,7 @@ static void launch_fwd(const FwdArgs& a, dim3 grid, cudaStream_t st) {
   const size_t smem = sizeof(fwd::Smem);
   cudaFuncSetAttribute(k_forward_core<REAL, SPIN0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  k_forward_core<REAL, SPIN0><<<grid, kCoreThreads, smem, st>>>(a);
+  k_forward_core<REAL, SPIN0><<<grid, fwd_threads<SPIN0>(), smem, st>>>(a);
 }
 
 void launch_forward_core(const FwdArgs& a, int ntiles, int nmaps, bool real, cudaStream_t st) {

@@ -50,7 +50,7 @@ __device__ __forceinline__ void rescale(double (&z)[NE], double (&zp)[NE], unsig
 }
 
 template <bool REAL, bool SPIN0>
-__global__ void __launch_bounds__(kCoreThreads, 1) k_inverse_core(InvArgs a) {
+__global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
   constexpr int NI = 4, NJ = 2, NE = NI * NJ;
   constexpr int NG = REAL ? 1 : 2;  // complex g values per column: f_{l,m} (+ f_{l,-m})
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -62,9 +62,9 @@ __global__ void __launch_bounds__(kCoreThreads, 1) k_inverse_core(InvArgs a) {
   const int r0 = tile.x, c0 = tile.y;
   const int lstart = max(r0, c0);
   const int nchunks = (L - lstart + kChunk - 1) / kChunk;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int lane = threadIdx.x & 31, wall = threadIdx.x >> 5;
 
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     for (int b = 0; b < inv::NB; b++) {
       mbar_init(&sm.full[b], 1);
       mbar_init(&sm.empty[b], kConsumerWarps);
@@ -73,7 +73,10 @@ __global__ void __launch_bounds__(kCoreThreads, 1) k_inverse_core(InvArgs a) {
   }
   __syncthreads();
 
-  if (w == kConsumerWarps) {
+  if (wall < 4) {
+    // warpgroup 0: warp 0 streams the stages, warps 1-3 retire; registers go to the consumers
+    setmaxnreg_dec<kProducerRegs>();
+    if (wall != 0) return;
     // ------------------------------------------------------------ producer
     const double2* rowtab = a.rowtab;
     const double2* gp = a.gp + (long long)blockIdx.y * a.g_stride;
@@ -105,6 +108,8 @@ __global__ void __launch_bounds__(kCoreThreads, 1) k_inverse_core(InvArgs a) {
   }
 
   // -------------------------------------------------------------- consumers
+  setmaxnreg_inc<kConsumerRegs>();
+  const int w = wall - 4, tid = threadIdx.x - 128;
   double2* __restrict__ out = a.out + (long long)blockIdx.y * a.out_stride;
   const int wr = w & 3, wc = w >> 2, r = lane & 3, c = lane >> 2, par = wr & 1;
   int rl[NI], cl[NJ], mp[NI], mm[NJ];
@@ -411,7 +416,7 @@ static void launch_inv(const InvArgs& a, dim3 grid, cudaStream_t st) {
   const size_t smem = sizeof(inv::Smem);
   cudaFuncSetAttribute(k_inverse_core<REAL, SPIN0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  k_inverse_core<REAL, SPIN0><<<grid, kCoreThreads, smem, st>>>(a);
+  k_inverse_core<REAL, SPIN0><<<grid, kCoreThreadsWS, smem, st>>>(a);
 }
 
 void launch_inverse_core(const InvArgs& a, int ntiles, int nmaps, bool real, cudaStream_t st) {
