@@ -2,7 +2,7 @@
 
 Drop-in for the reference package's transform path (torusht: forward,
 inverse, forward_real, inverse_real, HarmonicCoeffs, MwSignal, the error
-types), computed by hand-written sm_100a FP64 kernels + cuFFT behind the C ABI
+types), computed by hand-written sm_100a FP64 kernels (FFT stages included) behind the C ABI
 in include/mwsht.h.  See DESIGN.md.
 """
 
@@ -12,10 +12,11 @@ from .errors import (ContractViolationError, ConvergenceError, DeviceError,
 from .mw import (HarmonicCoeffs, MwSignal, Plan, check_band_limit, clear_plans, forward,
                  forward_batch, forward_real, get_plan, inverse, inverse_batch, inverse_real,
                  mw_grid_phis, mw_grid_thetas, reality_residual)
+from .pipeline import HostPipeline
 
 __all__ = [
     "HarmonicCoeffs", "MwSignal", "forward", "inverse", "forward_real", "inverse_real",
-    "forward_batch", "inverse_batch", "reality_residual", "check_band_limit",
+    "forward_batch", "inverse_batch", "reality_residual", "HostPipeline", "check_band_limit",
     "mw_grid_thetas", "mw_grid_phis", "Plan", "get_plan", "clear_plans",
     "TorushtError", "InvalidBandLimitError", "InvalidSpinError", "ContractViolationError",
     "UnsupportedDegreeError", "SymmetryError", "ConvergenceError", "DeviceError",

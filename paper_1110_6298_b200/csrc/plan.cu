@@ -31,7 +31,7 @@ void launch_inv_prescale(bool real, const double2* in, int in_mode, const double
 void launch_transpose(const double2* in, double2* out, int rows, int cols, cudaStream_t st);
 void launch_untranspose(bool real, const double2* S, double2* Out, int L, int N, long long ss,
                         long long os, int nm, cudaStream_t st);
-void launch_reality(const double2* f, int L, unsigned long long* worst, unsigned long long* peak,
+void launch_reality(const double2* f, int L, unsigned long long* red, unsigned long long* host,
                     cudaStream_t st);
 void fft_launch(int which, bool real, const fft::FftArgs& a, int nsm, cudaStream_t st);
 void fft_spectrum(const fft::FftArgs& a, const double2* kern, double2* spec, cudaStream_t st);
@@ -86,7 +86,9 @@ struct mwsht_plan {
           *rho = nullptr, *scratch = nullptr;
   double2 *bufA = nullptr, *bufB = nullptr, *bufG = nullptr;
   long long strideA = 0, strideB = 0, strideG = 0;
-  unsigned long long* red = nullptr;  // 2 slots for the reality check
+  unsigned long long* red = nullptr;       // 2 device slots for the reality check (kept zero)
+  unsigned long long* red_host = nullptr;  // host-mapped result of the reality check
+  unsigned long long* red_host_dev = nullptr;
   int own_launches = 0;
   bool timing = false;
   cudaEvent_t ev[2][3] = {};  // [forward|inverse][start, core start, core end]
@@ -660,6 +662,14 @@ int mwsht_plan_create(int L, int device, int max_batch, mwsht_plan** out) {
     mwsht_plan_destroy(p);
     return rc;
   }
+  e = cudaHostAlloc((void**)&p->red_host, 2 * sizeof(unsigned long long), cudaHostAllocMapped);
+  if (e == cudaSuccess)
+    e = cudaHostGetDevicePointer((void**)&p->red_host_dev, p->red_host, 0);
+  if (e == cudaSuccess) e = cudaMemset(p->red, 0, 2 * sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    mwsht_plan_destroy(p);
+    return fail(MWSHT_E_CUDA, "reality-check buffers", cudaGetErrorString(e));
+  }
   // the staging buffer's pad columns (m >= L) are read but never written: zero them once
   e = cudaMemset(p->bufG, 0, sizeof(double2) * p->strideG * max_batch);
   if (e != cudaSuccess) {
@@ -678,6 +688,7 @@ int mwsht_plan_destroy(mwsht_plan* p) {
     for (auto& e : d)
       if (e) cudaEventDestroy(e);
   for (void* q : p->allocs) cudaFree(q);
+  if (p->red_host) cudaFreeHost(p->red_host);
   delete p;
   return MWSHT_OK;
 }
@@ -727,12 +738,12 @@ int mwsht_reality_residual(mwsht_plan* p, const void* flm, double* worst_host, d
   if ((rc = check_plan(p))) return rc;
   std::lock_guard<std::mutex> lk(p->mu);
   cudaStream_t st = (cudaStream_t)stream;
-  CU(cudaMemsetAsync(p->red, 0, 2 * sizeof(unsigned long long), st));
-  launch_reality((const double2*)flm, p->L, p->red, p->red + 1, st);
+  launch_reality((const double2*)flm, p->L, p->red, p->red_host_dev, st);
   LAUNCHED(p);
-  unsigned long long h[2];
-  CU(cudaMemcpyAsync(h, p->red, sizeof h, cudaMemcpyDeviceToHost, st));
+  LAUNCHED(p);
   CU(cudaStreamSynchronize(st));
+  unsigned long long h[2];
+  memcpy(h, (const void*)p->red_host, sizeof h);
   double w, pk;
   memcpy(&w, &h[0], 8);
   memcpy(&pk, &h[1], 8);

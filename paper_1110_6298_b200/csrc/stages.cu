@@ -352,12 +352,24 @@ void launch_untranspose(bool real, const double2* S, double2* Out, int L, int N,
     k_untranspose<false><<<grid, block, 0, st>>>(S, Out, L, N, ss, os);
 }
 
-void launch_reality(const double2* f, int L, unsigned long long* worst, unsigned long long* peak,
+// Hands the two maxima to host-mapped memory with plain stores and re-zeroes the
+// device slots: the caller reads the result after a stream sync without a
+// copy-engine transfer (which would queue behind large D2H copies of other
+// streams, e.g. HostPipeline's).
+__global__ void k_reality_publish(unsigned long long* red, unsigned long long* host) {
+  host[0] = red[0];
+  host[1] = red[1];
+  red[0] = 0ull;
+  red[1] = 0ull;
+}
+
+void launch_reality(const double2* f, int L, unsigned long long* red, unsigned long long* host,
                     cudaStream_t st) {
   long long n = (long long)L * L;
   long long blocks = (n + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_reality<<<(unsigned)blocks, 256, 0, st>>>(f, L, worst, peak);
+  k_reality<<<(unsigned)blocks, 256, 0, st>>>(f, L, red, red + 1);
+  k_reality_publish<<<1, 1, 0, st>>>(red, host);
 }
 
 }  // namespace mwsht

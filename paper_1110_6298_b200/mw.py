@@ -110,10 +110,13 @@ class MwSignal:
         _freeze(self.samples)
 
 
-def _trusted(cls, band_limit, spin, data):
+def _trusted(cls, band_limit, spin, data, lead_checked=False):
     """Build a container from our own (already valid) output without re-validating
-    (avoids a device sync on torch outputs)."""
+    (avoids a device sync on torch outputs).  lead_checked: the l < |spin| zeros
+    were verified by the caller (e.g. on the host copy), inverse() skips them."""
     obj = object.__new__(cls)
+    if lead_checked:
+        object.__setattr__(obj, "_lead_checked", True)
     object.__setattr__(obj, "band_limit", band_limit)
     object.__setattr__(obj, "spin", spin)
     object.__setattr__(obj, "values" if cls is HarmonicCoeffs else "samples", data)
@@ -267,7 +270,7 @@ def inverse(coeffs, recursion="trapani"):
     """
     L, s = coeffs.band_limit, coeffs.spin
     _check_spin(L, s)
-    if _lead_nonzero(coeffs.values, s * s):
+    if not getattr(coeffs, "_lead_checked", False) and _lead_nonzero(coeffs.values, s * s):
         raise ContractViolationError(
             f"coefficients with degree below |spin|={abs(s)} must be zero on input to the "
             "inverse transform")

@@ -1,0 +1,61 @@
+"""HostPipeline: pipelined host-resident transforms give the same results as
+the per-call public API (which is itself parity-tested against the oracle)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1110_6298_b200 as mw
+from oracle import mw_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("kind", ["inverse", "forward", "roundtrip"])
+@pytest.mark.parametrize("L,spin,real", [(64, 0, False), (48, 2, False), (64, 0, True)])
+def test_pipeline_matches_api(kind, L, spin, real):
+    from paper_1110_6298_b200.pipeline import HostPipeline
+    nmaps = 5
+    N = 2 * L - 1
+    coeffs = [O.gaussian_real_coeffs(L, 10 + i) if real else O.gaussian_coeffs(L, spin, 10 + i)
+              for i in range(nmaps)]
+    inv = mw.inverse_real if real else mw.inverse
+    fwd = mw.forward_real if real else mw.forward
+    sigs = [np.asarray(inv(mw.HarmonicCoeffs(L, spin, c.copy())).samples) for c in coeffs]
+    if kind == "forward":
+        h_in = [torch.from_numpy(s.copy()).pin_memory() for s in sigs]
+        want = [np.asarray(fwd(mw.MwSignal(L, spin, s.copy())).values) for s in sigs]
+        h_out = [torch.empty(L * L, dtype=torch.complex128).pin_memory() for _ in range(nmaps)]
+    else:
+        h_in = [torch.from_numpy(c.copy()).pin_memory() for c in coeffs]
+        if kind == "inverse":
+            want = sigs
+            dt = torch.float64 if real else torch.complex128
+            h_out = [torch.empty((L, N), dtype=dt).pin_memory() for _ in range(nmaps)]
+        else:
+            want = [np.asarray(fwd(mw.MwSignal(L, spin, s.copy())).values) for s in sigs]
+            h_out = [torch.empty(L * L, dtype=torch.complex128).pin_memory() for _ in range(nmaps)]
+    pipe = HostPipeline(L, spin, kind=kind, real=real, device=0, depth=2)
+    for _ in range(2):  # twice: slots are reused
+        for i in range(nmaps):
+            pipe.submit(h_in[i], h_out[i])
+        pipe.synchronize()
+        for i in range(nmaps):
+            np.testing.assert_array_equal(h_out[i].numpy(), want[i])
+
+
+def test_pipeline_rejects_bad_shape():
+    from paper_1110_6298_b200.pipeline import HostPipeline
+    pipe = HostPipeline(16, 0, kind="roundtrip", device=0)
+    with pytest.raises(mw.ContractViolationError):
+        pipe.submit(torch.zeros(15 * 15, dtype=torch.complex128), torch.zeros(256))
+
+
+def test_pipeline_rejects_low_degree_for_spin():
+    from paper_1110_6298_b200.pipeline import HostPipeline
+    L = 16
+    pipe = HostPipeline(L, 2, kind="inverse", device=0)
+    bad = torch.zeros(L * L, dtype=torch.complex128)
+    bad[1] = 1.0
+    with pytest.raises(mw.ContractViolationError):
+        pipe.submit(bad, torch.empty((L, 2 * L - 1), dtype=torch.complex128))
