@@ -156,6 +156,12 @@ struct FftArgs {
 
 // ------------------------------------------------------- register budget
 namespace mwsht {
+// compile-time bool for generic-lambda dispatch
+template <bool B>
+struct BoolC {
+  static constexpr bool value = B;
+};
+
 template <int N>
 __device__ __forceinline__ void setmaxnreg_inc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N));

@@ -124,6 +124,9 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
     mm[j] = c0 + cl[j];
   }
 
+  int rl0 = rl[0], cl0 = cl[0];
+  asm volatile("" : "+r"(rl0), "+r"(cl0));
+
   // seeds: z^{l0} = Delta^{l0}_{m'm} / ((-1)^l0 lam_l0 u_l0(m) u_l0(m')), l0 = max(m', m),
   // Delta^{l0}_{m'm} = sign sqrt(C(2 l0, l0 + min))/2^l0, carried in exponent levels
   unsigned slv = 0;  // seed levels, 4 bits per chain
@@ -170,80 +173,17 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
   for (int k = 0; k < nchunks; k++) {
     const int b = k % inv::NB, lc = lstart + k * kChunk, ns = min(kChunk, L - lc);
     mbar_wait(&sm.full[b], (k / inv::NB) & 1);
+    // rl[i] = rl0 + 8 i, cl[j] = cl0 + 8 j: one base pointer per array and chunk,
+    // constant offsets per entry (rl0/cl0 opaque: never rematerialised from %tid)
     const inv::Stage& S = sm.st[b];
+    const double2* rowp = &S.row[0][0] + rl0;
+    const double* colp = &S.colc[0][0] + cl0;
+    const double2* gpp = &S.gp[0][0] + cl0;
+    const double2* gnp = &S.gn[0][0] + cl0;
 
     if (warp_has && wl0_min < lc + ns) {
       if (!fast) fast = (wl0_max < lc) && __all_sync(0xffffffffu, lv == 0);
-      if (fast) {
-        // ------------------------------------------------------- steady state
-        auto rec_step = [&](int s) {
-          double2 rp[NI];
-          double cc[NJ];
-#pragma unroll
-          for (int i = 0; i < NI; i++) rp[i] = S.row[s][rl[i]];
-#pragma unroll
-          for (int j = 0; j < NJ; j++) cc[j] = S.colc[s][cl[j]];
-#pragma unroll
-          for (int i = 0; i < NI; i++)
-#pragma unroll
-            for (int j = 0; j < NJ; j++) {
-              const int e = i * NJ + j;
-              const double zn = fma(rp[i].x * cc[j], z[e], -zp[e]);
-              zp[e] = z[e];
-              z[e] = zn;
-            }
-        };
-        auto full_step = [&](int s) {
-          double2 rp[NI];
-          double cc[NJ];
-          double2 g[NJ][NG];
-#pragma unroll
-          for (int i = 0; i < NI; i++) rp[i] = S.row[s][rl[i]];
-#pragma unroll
-          for (int j = 0; j < NJ; j++) {
-            cc[j] = S.colc[s][cl[j]];
-            g[j][0] = S.gp[s][cl[j]];
-            if (!REAL) g[j][NG - 1] = S.gn[s][cl[j]];
-          }
-#pragma unroll
-          for (int i = 0; i < NI; i++)
-#pragma unroll
-            for (int j = 0; j < NJ; j++) {
-              const int e = i * NJ + j;
-              const double t = z[e] * rp[i].y;
-#pragma unroll
-              for (int k2 = 0; k2 < NG; k2++) {
-                acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
-                acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
-              }
-              const double zn = fma(rp[i].x * cc[j], z[e], -zp[e]);
-              zp[e] = z[e];
-              z[e] = zn;
-            }
-        };
-        if (SPIN0) {
-          // lc is even (tile corners are multiples of 32): pairs (even l, odd l)
-          int s = 0;
-          for (; s + 1 < ns; s += 2) {
-            if (par == 0) {
-              full_step(s);
-              rec_step(s + 1);
-            } else {
-              rec_step(s);
-              full_step(s + 1);
-            }
-          }
-          if (s < ns) {
-            if (par == 0)
-              full_step(s);
-            else
-              rec_step(s);
-          }
-        } else {
-#pragma unroll 2
-          for (int s = 0; s < ns; s++) full_step(s);
-        }
-      } else if (wl0_max >= lc) {
+      if (!fast && wl0_max >= lc) {
         // --------------------------------- ramp: seed injection, levels, masking
         for (int s = 0; s < ns; s++) {
           const int l = lc + s;
@@ -251,12 +191,12 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
           double cc[NJ];
           double2 g[NJ][NG];
 #pragma unroll
-          for (int i = 0; i < NI; i++) rp[i] = S.row[s][rl[i]];
+          for (int i = 0; i < NI; i++) rp[i] = rowp[s * inv::R + 8 * i];
 #pragma unroll
           for (int j = 0; j < NJ; j++) {
-            cc[j] = S.colc[s][cl[j]];
-            g[j][0] = S.gp[s][cl[j]];
-            if (!REAL) g[j][NG - 1] = S.gn[s][cl[j]];
+            cc[j] = colp[s * inv::C + 8 * j];
+            g[j][0] = gpp[s * inv::C + 8 * j];
+            if (!REAL) g[j][NG - 1] = gnp[s * inv::C + 8 * j];
           }
 #pragma unroll
           for (int i = 0; i < NI; i++)
@@ -304,42 +244,27 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
           if (lv && (s & 3) == 3) rescale(z, zp, lv);
         }
       } else {
-        // all chains started; some still carry exponent levels.  A chain that
-        // reaches level 0 inside this chunk is still below 2^-568 (its true
-        // value grows at most 4x per degree), so contributions start at the
-        // next chunk without loss; masking is per chunk, not per step.
-        unsigned live = 0;  // bit e: chain e at true scale for the whole chunk
+        // ------------------------------------------------------- steady state
+        // Every chain has started.  Chains still carrying exponent levels
+        // (lv != 0: true value below 2^-568) are masked out of the contraction
+        // for the whole chunk; one rescale check at the chunk end suffices
+        // (a chain grows at most 4x per degree: 2^32 per chunk from <= 2^200),
+        // and a chain that reaches level 0 inside a chunk contributes from the
+        // next one without loss.  fast: no chain in the warp carries a level.
+        unsigned live = 0xffffffffu;
+        if (!fast) {
+          live = 0;
 #pragma unroll
-        for (int e = 0; e < NE; e++) live |= (((lv >> (4 * e)) & 15u) == 0) ? (1u << e) : 0u;
-        const bool anylive = __any_sync(0xffffffffu, live != 0);
-        for (int s = 0; s < ns; s++) {
-          const int l = lc + s;
+          for (int e = 0; e < NE; e++) live |= (((lv >> (4 * e)) & 15u) == 0) ? (1u << e) : 0u;
+        }
+        const bool contract = fast || __any_sync(0xffffffffu, live != 0);
+        auto rec_step = [&](int s) {
           double2 rp[NI];
           double cc[NJ];
 #pragma unroll
-          for (int i = 0; i < NI; i++) rp[i] = S.row[s][rl[i]];
+          for (int i = 0; i < NI; i++) rp[i] = rowp[s * inv::R + 8 * i];
 #pragma unroll
-          for (int j = 0; j < NJ; j++) cc[j] = S.colc[s][cl[j]];
-          if (anylive && (!SPIN0 || ((l & 1) == par))) {
-            double2 g[NJ][NG];
-#pragma unroll
-            for (int j = 0; j < NJ; j++) {
-              g[j][0] = S.gp[s][cl[j]];
-              if (!REAL) g[j][NG - 1] = S.gn[s][cl[j]];
-            }
-#pragma unroll
-            for (int i = 0; i < NI; i++)
-#pragma unroll
-              for (int j = 0; j < NJ; j++) {
-                const int e = i * NJ + j;
-                const double t = ((live >> e) & 1u) ? z[e] * rp[i].y : 0.0;
-#pragma unroll
-                for (int k2 = 0; k2 < NG; k2++) {
-                  acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
-                  acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
-                }
-              }
-          }
+          for (int j = 0; j < NJ; j++) cc[j] = colp[s * inv::C + 8 * j];
 #pragma unroll
           for (int i = 0; i < NI; i++)
 #pragma unroll
@@ -349,7 +274,69 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
               zp[e] = z[e];
               z[e] = zn;
             }
-          if ((s & 3) == 3) rescale(z, zp, lv);
+        };
+        auto full_step = [&](auto masked, int s) {
+          double2 rp[NI];
+          double cc[NJ];
+          double2 g[NJ][NG];
+#pragma unroll
+          for (int i = 0; i < NI; i++) rp[i] = rowp[s * inv::R + 8 * i];
+#pragma unroll
+          for (int j = 0; j < NJ; j++) {
+            cc[j] = colp[s * inv::C + 8 * j];
+            g[j][0] = gpp[s * inv::C + 8 * j];
+            if (!REAL) g[j][NG - 1] = gnp[s * inv::C + 8 * j];
+          }
+#pragma unroll
+          for (int i = 0; i < NI; i++)
+#pragma unroll
+            for (int j = 0; j < NJ; j++) {
+              const int e = i * NJ + j;
+              double t = z[e] * rp[i].y;
+              if (decltype(masked)::value) t = ((live >> e) & 1u) ? t : 0.0;
+#pragma unroll
+              for (int k2 = 0; k2 < NG; k2++) {
+                acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
+                acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
+              }
+              const double zn = fma(rp[i].x * cc[j], z[e], -zp[e]);
+              zp[e] = z[e];
+              z[e] = zn;
+            }
+        };
+        auto run = [&](auto masked) {
+          if (SPIN0) {
+            // lc is even (tile corners are multiples of 32): pairs (even l, odd l)
+            int s = 0;
+#pragma unroll 2
+            for (; s + 1 < ns; s += 2) {
+              if (par == 0) {
+                full_step(masked, s);
+                rec_step(s + 1);
+              } else {
+                rec_step(s);
+                full_step(masked, s + 1);
+              }
+            }
+            if (s < ns) {
+              if (par == 0)
+                full_step(masked, s);
+              else
+                rec_step(s);
+            }
+          } else {
+#pragma unroll 2
+            for (int s = 0; s < ns; s++) full_step(masked, s);
+          }
+        };
+        if (fast) {
+          run(BoolC<false>());
+        } else {
+          if (contract)
+            run(BoolC<true>());
+          else
+            for (int s = 0; s < ns; s++) rec_step(s);
+          rescale(z, zp, lv);
         }
       }
     }
