@@ -133,6 +133,9 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
     md[j] = (double)mm[j];
   }
 
+  int rl0 = rl[0], cl0 = cl[0];
+  asm volatile("" : "+r"(rl0), "+r"(cl0));
+
   // seeds: y_l = Delta^l_{l,m} / (A(0) Bt(2l)), Delta^l_{l,m} = (-1)^(l-m) sqrt(C(2l,l+m))/2^l
   unsigned slv = 0;
 #pragma unroll
@@ -173,84 +176,25 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
   for (int k = 0; k < nchunks; k++) {
     const int b = k % fwd::NB, mc = mu_top - k * kChunk, ns = min(kChunk, mc + 1);
     mbar_wait(&sm.full[b], (k / fwd::NB) & 1);
+    // rl[i] = rl0 + 8 i, cl[j] = cl0 + 8 j: one base pointer per array and chunk
     const fwd::Stage& S = sm.st[b];
+    const double2* rowp = &S.q[0][0] + rl0;
+    const double2* gpp = &S.gp[0][0] + cl0;
+    const double2* gnp = &S.gn[0][0] + cl0;
 
     if (warp_has && wrow_hi >= mc - ns + 1) {
       if (!fast) fast = (mc < wl_min) && __all_sync(0xffffffffu, lv == 0);
-      if (fast) {
-        auto rec_step = [&](int s) {
-          double2 qp[NI];
-#pragma unroll
-          for (int i = 0; i < NI; i++) qp[i] = S.q[s][rl[i]];
-#pragma unroll
-          for (int i = 0; i < NI; i++)
-#pragma unroll
-            for (int j = 0; j < NJ; j++) {
-              const int e = i * NJ + j;
-              const double yn = fma(md[j] * qp[i].x, y[e], -y1[e]);
-              y1[e] = y[e];
-              y[e] = yn;
-            }
-        };
-        auto full_step = [&](int s) {
-          double2 qp[NI], g[NJ][NG];
-#pragma unroll
-          for (int i = 0; i < NI; i++) qp[i] = S.q[s][rl[i]];
-#pragma unroll
-          for (int j = 0; j < NJ; j++) {
-            g[j][0] = S.gp[s][cl[j]];
-            if (!REAL) g[j][NG - 1] = S.gn[s][cl[j]];
-          }
-#pragma unroll
-          for (int i = 0; i < NI; i++)
-#pragma unroll
-            for (int j = 0; j < NJ; j++) {
-              const int e = i * NJ + j;
-              const double t = y[e] * qp[i].y;
-#pragma unroll
-              for (int k2 = 0; k2 < NG; k2++) {
-                acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
-                acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
-              }
-              const double yn = fma(md[j] * qp[i].x, y[e], -y1[e]);
-              y1[e] = y[e];
-              y[e] = yn;
-            }
-        };
-        if (SPIN0) {
-          // contraction when m' has the warp's degree parity
-          const bool first_full = ((mc & 1) == par);
-          int s = 0;
-          for (; s + 1 < ns; s += 2) {
-            if (first_full) {
-              full_step(s);
-              rec_step(s + 1);
-            } else {
-              rec_step(s);
-              full_step(s + 1);
-            }
-          }
-          if (s < ns) {
-            if (first_full)
-              full_step(s);
-            else
-              rec_step(s);
-          }
-        } else {
-#pragma unroll 2
-          for (int s = 0; s < ns; s++) full_step(s);
-        }
-      } else if (mc >= wl_min) {
+      if (!fast && mc >= wl_min) {
         // ---------------------------- ramp: chains starting, levels, masking
         for (int s = 0; s < ns; s++) {
           const int mu = mc - s;
           double2 qp[NI], g[NJ][NG];
 #pragma unroll
-          for (int i = 0; i < NI; i++) qp[i] = S.q[s][rl[i]];
+          for (int i = 0; i < NI; i++) qp[i] = rowp[s * fwd::R + 8 * i];
 #pragma unroll
           for (int j = 0; j < NJ; j++) {
-            g[j][0] = S.gp[s][cl[j]];
-            if (!REAL) g[j][NG - 1] = S.gn[s][cl[j]];
+            g[j][0] = gpp[s * fwd::C + 8 * j];
+            if (!REAL) g[j][NG - 1] = gnp[s * fwd::C + 8 * j];
           }
           bool contrib = false;
 #pragma unroll
@@ -291,37 +235,23 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
           if (lv && (s & 3) == 3) rescale(y, y1, lv);
         }
       } else {
-        // all chains started; some still carry exponent levels (masking per
-        // chunk is lossless: a chain reaching level 0 is still below 2^-568)
-        unsigned live = 0;
+        // ------------------------------------------------------- steady state
+        // Every chain has started.  Chains still carrying exponent levels are
+        // masked out of the contraction for the whole chunk and checked for a
+        // rescale once at its end (no overflow: stored values stay far below
+        // 2^1023 within 16 steps of 2^200; a chain reaching level 0 inside the
+        // chunk is below 2^-464 there and contributes from the next chunk).
+        unsigned live = 0xffffffffu;
+        if (!fast) {
+          live = 0;
 #pragma unroll
-        for (int e = 0; e < NE; e++) live |= (((lv >> (4 * e)) & 15u) == 0) ? (1u << e) : 0u;
-        const bool anylive = __any_sync(0xffffffffu, live != 0);
-        for (int s = 0; s < ns; s++) {
-          const int mu = mc - s;
+          for (int e = 0; e < NE; e++) live |= (((lv >> (4 * e)) & 15u) == 0) ? (1u << e) : 0u;
+        }
+        const bool contract = fast || __any_sync(0xffffffffu, live != 0);
+        auto rec_step = [&](int s) {
           double2 qp[NI];
 #pragma unroll
-          for (int i = 0; i < NI; i++) qp[i] = S.q[s][rl[i]];
-          if (anylive && (!SPIN0 || ((mu & 1) == par))) {
-            double2 g[NJ][NG];
-#pragma unroll
-            for (int j = 0; j < NJ; j++) {
-              g[j][0] = S.gp[s][cl[j]];
-              if (!REAL) g[j][NG - 1] = S.gn[s][cl[j]];
-            }
-#pragma unroll
-            for (int i = 0; i < NI; i++)
-#pragma unroll
-              for (int j = 0; j < NJ; j++) {
-                const int e = i * NJ + j;
-                const double t = ((live >> e) & 1u) ? y[e] * qp[i].y : 0.0;
-#pragma unroll
-                for (int k2 = 0; k2 < NG; k2++) {
-                  acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
-                  acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
-                }
-              }
-          }
+          for (int i = 0; i < NI; i++) qp[i] = rowp[s * fwd::R + 8 * i];
 #pragma unroll
           for (int i = 0; i < NI; i++)
 #pragma unroll
@@ -331,7 +261,66 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
               y1[e] = y[e];
               y[e] = yn;
             }
-          if ((s & 3) == 3) rescale(y, y1, lv);
+        };
+        auto full_step = [&](auto masked, int s) {
+          double2 qp[NI], g[NJ][NG];
+#pragma unroll
+          for (int i = 0; i < NI; i++) qp[i] = rowp[s * fwd::R + 8 * i];
+#pragma unroll
+          for (int j = 0; j < NJ; j++) {
+            g[j][0] = gpp[s * fwd::C + 8 * j];
+            if (!REAL) g[j][NG - 1] = gnp[s * fwd::C + 8 * j];
+          }
+#pragma unroll
+          for (int i = 0; i < NI; i++)
+#pragma unroll
+            for (int j = 0; j < NJ; j++) {
+              const int e = i * NJ + j;
+              double t = y[e] * qp[i].y;
+              if (decltype(masked)::value) t = ((live >> e) & 1u) ? t : 0.0;
+#pragma unroll
+              for (int k2 = 0; k2 < NG; k2++) {
+                acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
+                acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
+              }
+              const double yn = fma(md[j] * qp[i].x, y[e], -y1[e]);
+              y1[e] = y[e];
+              y[e] = yn;
+            }
+        };
+        auto run = [&](auto masked) {
+          if (SPIN0) {
+            // contraction when m' has the warp's degree parity
+            const bool first_full = ((mc & 1) == par);
+            int s = 0;
+            for (; s + 1 < ns; s += 2) {
+              if (first_full) {
+                full_step(masked, s);
+                rec_step(s + 1);
+              } else {
+                rec_step(s);
+                full_step(masked, s + 1);
+              }
+            }
+            if (s < ns) {
+              if (first_full)
+                full_step(masked, s);
+              else
+                rec_step(s);
+            }
+          } else {
+#pragma unroll 2
+            for (int s = 0; s < ns; s++) full_step(masked, s);
+          }
+        };
+        if (fast) {
+          run(BoolC<false>());
+        } else {
+          if (contract)
+            run(BoolC<true>());
+          else
+            for (int s = 0; s < ns; s++) rec_step(s);
+          rescale(y, y1, lv);
         }
       }
     }
