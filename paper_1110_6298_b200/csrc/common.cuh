@@ -156,6 +156,15 @@ struct FftArgs {
 
 // ------------------------------------------------------- register budget
 namespace mwsht {
+// bit e set when chain e (4-bit level nibble e of lv) is at level 0
+template <int NE>
+__device__ __forceinline__ unsigned level_zero_mask(unsigned lv) {
+  unsigned m = 0;
+#pragma unroll
+  for (int e = 0; e < NE; e++) m |= (((lv >> (4 * e)) & 15u) == 0) ? (1u << e) : 0u;
+  return m;
+}
+
 // compile-time bool for generic-lambda dispatch
 template <bool B>
 struct BoolC {

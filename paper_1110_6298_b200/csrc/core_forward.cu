@@ -186,40 +186,47 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
       if (!fast) fast = (mc < wl_min) && __all_sync(0xffffffffu, lv == 0);
       if (!fast && mc >= wl_min) {
         // ---------------------------- ramp: chains starting, levels, masking
+        // Chains not yet started are exactly 0; chains carrying exponent levels
+        // are masked via `live`, which changes only at a start or a rescale.
+        unsigned live = level_zero_mask<NE>(lv);
         for (int s = 0; s < ns; s++) {
           const int mu = mc - s;
-          double2 qp[NI], g[NJ][NG];
+          double2 qp[NI];
 #pragma unroll
           for (int i = 0; i < NI; i++) qp[i] = rowp[s * fwd::R + 8 * i];
+          if (mu >= ll[0] && mu <= ll[NI - 1]) {
 #pragma unroll
-          for (int j = 0; j < NJ; j++) {
-            g[j][0] = gpp[s * fwd::C + 8 * j];
-            if (!REAL) g[j][NG - 1] = gnp[s * fwd::C + 8 * j];
+            for (int i = 0; i < NI; i++)
+              if (mu == ll[i]) {  // chains start with y_{l+1} = 0
+#pragma unroll
+                for (int j = 0; j < NJ; j++) {
+                  const int e = i * NJ + j;
+                  y[e] = sm.seedy[e][tid];
+                  y1[e] = 0.0;
+                  lv |= slv & (15u << (4 * e));
+                }
+              }
+            live = level_zero_mask<NE>(lv);
           }
-          bool contrib = false;
-#pragma unroll
-          for (int i = 0; i < NI; i++)
+          if ((!SPIN0 || ((mu & 1) == par)) && mu <= wrow_hi) {
+            double2 g[NJ][NG];
 #pragma unroll
             for (int j = 0; j < NJ; j++) {
-              const int e = i * NJ + j;
-              if (mu == ll[i]) {  // chains start with y_{l+1} = 0
-                y[e] = sm.seedy[e][tid];
-                y1[e] = 0.0;
-                lv |= slv & (15u << (4 * e));
-              }
-              contrib |= (mu <= ll[i]) && ((lv >> (4 * e)) & 15u) == 0;
+              g[j][0] = gpp[s * fwd::C + 8 * j];
+              if (!REAL) g[j][NG - 1] = gnp[s * fwd::C + 8 * j];
             }
-          if ((!SPIN0 || ((mu & 1) == par)) && __any_sync(0xffffffffu, contrib)) {
 #pragma unroll
             for (int i = 0; i < NI; i++)
 #pragma unroll
               for (int j = 0; j < NJ; j++) {
                 const int e = i * NJ + j;
-                const double t = ((lv >> (4 * e)) & 15u) ? 0.0 : y[e] * qp[i].y;
+                if ((live >> e) & 1u) {
+                  const double t = y[e] * qp[i].y;
 #pragma unroll
-                for (int k2 = 0; k2 < NG; k2++) {
-                  acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
-                  acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
+                  for (int k2 = 0; k2 < NG; k2++) {
+                    acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
+                    acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
+                  }
                 }
               }
           }
@@ -232,7 +239,10 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
               y1[e] = y[e];
               y[e] = yn;
             }
-          if (lv && (s & 3) == 3) rescale(y, y1, lv);
+          if (lv && (s & 3) == 3) {
+            rescale(y, y1, lv);
+            live = level_zero_mask<NE>(lv);
+          }
         }
       } else {
         // ------------------------------------------------------- steady state

@@ -185,50 +185,52 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
       if (!fast) fast = (wl0_max < lc) && __all_sync(0xffffffffu, lv == 0);
       if (!fast && wl0_max >= lc) {
         // --------------------------------- ramp: seed injection, levels, masking
+        // Chains not yet started are exactly 0 and contribute nothing; chains
+        // carrying exponent levels (true value below 2^-568) are masked via
+        // `live`, which changes only at an injection or a rescale.
+        const int tl0min = max(mp[0], mm[0]), tl0max = max(mp[NI - 1], mm[NJ - 1]);
+        unsigned live = level_zero_mask<NE>(lv);
         for (int s = 0; s < ns; s++) {
           const int l = lc + s;
           double2 rp[NI];
           double cc[NJ];
-          double2 g[NJ][NG];
 #pragma unroll
           for (int i = 0; i < NI; i++) rp[i] = rowp[s * inv::R + 8 * i];
 #pragma unroll
-          for (int j = 0; j < NJ; j++) {
-            cc[j] = colp[s * inv::C + 8 * j];
-            g[j][0] = gpp[s * inv::C + 8 * j];
-            if (!REAL) g[j][NG - 1] = gnp[s * inv::C + 8 * j];
-          }
-#pragma unroll
-          for (int i = 0; i < NI; i++)
-#pragma unroll
-            for (int j = 0; j < NJ; j++) {
-              const int e = i * NJ + j;
-              if (l == max(mp[i], mm[j])) {  // chains start with z^{l0-1} = 0
-                z[e] = sm.seedz[e][tid];
-                zp[e] = 0.0;
-                lv |= slv & (15u << (4 * e));
-              }
-            }
-          // chains not started are exactly 0; chains below 2^-568 (level > 0) are masked
-          bool contrib = false;
-#pragma unroll
-          for (int i = 0; i < NI; i++)
-#pragma unroll
-            for (int j = 0; j < NJ; j++) {
-              const int e = i * NJ + j;
-              contrib |= (l >= max(mp[i], mm[j])) && ((lv >> (4 * e)) & 15u) == 0;
-            }
-          if ((!SPIN0 || ((l & 1) == par)) && __any_sync(0xffffffffu, contrib)) {
+          for (int j = 0; j < NJ; j++) cc[j] = colp[s * inv::C + 8 * j];
+          if (l >= tl0min && l <= tl0max) {
 #pragma unroll
             for (int i = 0; i < NI; i++)
 #pragma unroll
               for (int j = 0; j < NJ; j++) {
                 const int e = i * NJ + j;
-                const double t = ((lv >> (4 * e)) & 15u) ? 0.0 : z[e] * rp[i].y;
+                if (l == max(mp[i], mm[j])) {  // chains start with z^{l0-1} = 0
+                  z[e] = sm.seedz[e][tid];
+                  zp[e] = 0.0;
+                  lv |= slv & (15u << (4 * e));
+                }
+              }
+            live = level_zero_mask<NE>(lv);
+          }
+          if ((!SPIN0 || ((l & 1) == par)) && l >= wl0_min) {
+            double2 g[NJ][NG];
 #pragma unroll
-                for (int k2 = 0; k2 < NG; k2++) {
-                  acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
-                  acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
+            for (int j = 0; j < NJ; j++) {
+              g[j][0] = gpp[s * inv::C + 8 * j];
+              if (!REAL) g[j][NG - 1] = gnp[s * inv::C + 8 * j];
+            }
+#pragma unroll
+            for (int i = 0; i < NI; i++)
+#pragma unroll
+              for (int j = 0; j < NJ; j++) {
+                const int e = i * NJ + j;
+                if ((live >> e) & 1u) {
+                  const double t = z[e] * rp[i].y;
+#pragma unroll
+                  for (int k2 = 0; k2 < NG; k2++) {
+                    acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
+                    acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
+                  }
                 }
               }
           }
@@ -241,7 +243,10 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
               zp[e] = z[e];
               z[e] = zn;
             }
-          if (lv && (s & 3) == 3) rescale(z, zp, lv);
+          if (lv && (s & 3) == 3) {
+            rescale(z, zp, lv);
+            live = level_zero_mask<NE>(lv);
+          }
         }
       } else {
         // ------------------------------------------------------- steady state
