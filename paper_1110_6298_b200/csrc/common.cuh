@@ -154,6 +154,20 @@ struct FftArgs {
 
 }  // namespace mwsht
 
+// ------------------------------------------------------- blocked layouts
+// The cores' per-degree inputs are stored column-blocked so that one chunk of
+// kChunk consecutive steps of a tile is ONE contiguous TMA bulk copy:
+//   blk<W>(step, col, L) = (col / W) * (L * W) + step * W + col % W,
+// W = kTileCols (32) for column-indexed data (C_l(m), the staging planes)
+// and kTileRows (64) for the row tables.  A plane of L steps x ldw columns
+// (ldw a multiple of 64) keeps its L * ldw size.
+namespace mwsht {
+template <int W>
+__host__ __device__ __forceinline__ long long blk(int step, int col, int L) {
+  return (long long)(col / W) * ((long long)L * W) + (long long)step * W + (col % W);
+}
+}  // namespace mwsht
+
 // ------------------------------------------------------- register budget
 namespace mwsht {
 // bit e set when chain e (4-bit level nibble e of lv) is at level 0

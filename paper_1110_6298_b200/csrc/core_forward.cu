@@ -89,26 +89,22 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
     // ------------------------------------------------------------ producer
     const double2* gp = a.gf + (long long)blockIdx.y * a.in_stride;
     const double2* gn = gp + (long long)L * Lp;
-    for (int k = 0; k < nchunks; k++) {
-      const int b = k % fwd::NB, mc = mu_top - k * kChunk, ns = min(kChunk, mc + 1);
-      if (k >= fwd::NB) mbar_wait(&sm.empty[b], ((k / fwd::NB) - 1) & 1);
-      if (lane == 0) {
+    // blocked layouts (common.cuh): the chunk's steps mu = mc .. mc-ns+1 are one
+    // contiguous block (ascending mu), placed in stage rows CH-ns .. CH-1 so
+    // that step s (mu = mc - s) always sits in row CH-1-s
+    if (lane == 0) {
+      for (int k = 0; k < nchunks; k++) {
+        const int b = k % fwd::NB, mc = mu_top - k * kChunk, ns = min(kChunk, mc + 1);
+        if (k >= fwd::NB) mbar_wait(&sm.empty[b], ((k / fwd::NB) - 1) & 1);
         fence_proxy_async();
         mbar_arrive_expect_tx(&sm.full[b], ns * (fwd::R * 16u + NG * fwd::C * 16u));
-      }
-      __syncwarp();
-      fwd::Stage& S = sm.st[b];
-      if (lane < kChunk) {
-        if (lane < ns)
-          bulk_g2s(&S.q[lane][0], a.rowtab + (long long)(mc - lane) * Lp + l0b, fwd::R * 16,
-                   &sm.full[b]);
-      } else {
-        const int s = lane - kChunk;
-        if (s < ns) {
-          const long long off = (long long)(mc - s) * Lp + c0;
-          bulk_g2s(&S.gp[s][0], gp + off, fwd::C * 16, &sm.full[b]);
-          if (!REAL) bulk_g2s(&S.gn[s][0], gn + off, fwd::C * 16, &sm.full[b]);
-        }
+        fwd::Stage& S = sm.st[b];
+        const int mlo = mc - ns + 1;
+        const long long oc = blk<fwd::C>(mlo, c0, L);
+        bulk_g2s(&S.q[fwd::CH - ns][0], a.rowtab + blk<fwd::R>(mlo, l0b, L), ns * fwd::R * 16,
+                 &sm.full[b]);
+        bulk_g2s(&S.gp[fwd::CH - ns][0], gp + oc, ns * fwd::C * 16, &sm.full[b]);
+        if (!REAL) bulk_g2s(&S.gn[fwd::CH - ns][0], gn + oc, ns * fwd::C * 16, &sm.full[b]);
       }
     }
     return;
@@ -178,9 +174,9 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
     mbar_wait(&sm.full[b], (k / fwd::NB) & 1);
     // rl[i] = rl0 + 8 i, cl[j] = cl0 + 8 j: one base pointer per array and chunk
     const fwd::Stage& S = sm.st[b];
-    const double2* rowp = &S.q[0][0] + rl0;
-    const double2* gpp = &S.gp[0][0] + cl0;
-    const double2* gnp = &S.gn[0][0] + cl0;
+    const double2* rowp = &S.q[fwd::CH - 1][0] + rl0;  // step s at row CH-1-s
+    const double2* gpp = &S.gp[fwd::CH - 1][0] + cl0;
+    const double2* gnp = &S.gn[fwd::CH - 1][0] + cl0;
 
     if (warp_has && wrow_hi >= mc - ns + 1) {
       if (!fast) fast = (mc < wl_min) && __all_sync(0xffffffffu, lv == 0);
@@ -193,7 +189,7 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
           const int mu = mc - s;
           double2 qp[NI];
 #pragma unroll
-          for (int i = 0; i < NI; i++) qp[i] = rowp[s * fwd::R + 8 * i];
+          for (int i = 0; i < NI; i++) qp[i] = rowp[-s * fwd::R + 8 * i];
           if (mu >= ll[0] && mu <= ll[NI - 1]) {
 #pragma unroll
             for (int i = 0; i < NI; i++)
@@ -212,8 +208,8 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
             double2 g[NJ][NG];
 #pragma unroll
             for (int j = 0; j < NJ; j++) {
-              g[j][0] = gpp[s * fwd::C + 8 * j];
-              if (!REAL) g[j][NG - 1] = gnp[s * fwd::C + 8 * j];
+              g[j][0] = gpp[-s * fwd::C + 8 * j];
+              if (!REAL) g[j][NG - 1] = gnp[-s * fwd::C + 8 * j];
             }
 #pragma unroll
             for (int i = 0; i < NI; i++)
@@ -261,7 +257,7 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
         auto rec_step = [&](int s) {
           double2 qp[NI];
 #pragma unroll
-          for (int i = 0; i < NI; i++) qp[i] = rowp[s * fwd::R + 8 * i];
+          for (int i = 0; i < NI; i++) qp[i] = rowp[-s * fwd::R + 8 * i];
 #pragma unroll
           for (int i = 0; i < NI; i++)
 #pragma unroll
@@ -275,11 +271,11 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
         auto full_step = [&](auto masked, int s) {
           double2 qp[NI], g[NJ][NG];
 #pragma unroll
-          for (int i = 0; i < NI; i++) qp[i] = rowp[s * fwd::R + 8 * i];
+          for (int i = 0; i < NI; i++) qp[i] = rowp[-s * fwd::R + 8 * i];
 #pragma unroll
           for (int j = 0; j < NJ; j++) {
-            g[j][0] = gpp[s * fwd::C + 8 * j];
-            if (!REAL) g[j][NG - 1] = gnp[s * fwd::C + 8 * j];
+            g[j][0] = gpp[-s * fwd::C + 8 * j];
+            if (!REAL) g[j][NG - 1] = gnp[-s * fwd::C + 8 * j];
           }
 #pragma unroll
           for (int i = 0; i < NI; i++)

@@ -15,7 +15,8 @@
 // plan table (kap_l C_l(m'), W_l(m')), rows of C_l(m), and rows of the
 // pre-scaled coefficients c_l u_l(m) f_{l,+-m} -- with TMA bulk copies
 // (cp.async.bulk -> UBLKCP) into a 4-deep ring of 16-degree stages guarded by
-// full/empty mbarriers.  Consumer warps never meet at a CTA barrier.
+// full/empty mbarriers (one bulk copy per array and stage: the tables and
+// staging planes are column-blocked, common.cuh).  Consumer warps never meet at a CTA barrier.
 #include "common.cuh"
 
 namespace mwsht {
@@ -81,27 +82,19 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
     const double2* rowtab = a.rowtab;
     const double2* gp = a.gp + (long long)blockIdx.y * a.g_stride;
     const double2* gn = gp + (long long)L * Lp;
-    for (int k = 0; k < nchunks; k++) {
-      const int b = k % inv::NB, lc = lstart + k * kChunk, ns = min(kChunk, L - lc);
-      if (k >= inv::NB) mbar_wait(&sm.empty[b], ((k / inv::NB) - 1) & 1);
-      if (lane == 0) {
+    // blocked layouts (common.cuh): a chunk is one contiguous copy per array
+    if (lane == 0) {
+      for (int k = 0; k < nchunks; k++) {
+        const int b = k % inv::NB, lc = lstart + k * kChunk, ns = min(kChunk, L - lc);
+        if (k >= inv::NB) mbar_wait(&sm.empty[b], ((k / inv::NB) - 1) & 1);
         fence_proxy_async();
         mbar_arrive_expect_tx(&sm.full[b], ns * (inv::R * 16u + inv::C * 8u + NG * inv::C * 16u));
-      }
-      __syncwarp();
-      inv::Stage& S = sm.st[b];
-      if (lane < kChunk) {
-        if (lane < ns)
-          bulk_g2s(&S.row[lane][0], rowtab + (long long)(lc + lane) * Lp + r0, inv::R * 16,
-                   &sm.full[b]);
-      } else {
-        const int s = lane - kChunk;
-        if (s < ns) {
-          const long long off = (long long)(lc + s) * Lp + c0;
-          bulk_g2s(&S.colc[s][0], a.colc + off, inv::C * 8, &sm.full[b]);
-          bulk_g2s(&S.gp[s][0], gp + off, inv::C * 16, &sm.full[b]);
-          if (!REAL) bulk_g2s(&S.gn[s][0], gn + off, inv::C * 16, &sm.full[b]);
-        }
+        inv::Stage& S = sm.st[b];
+        const long long oc = blk<inv::C>(lc, c0, L);
+        bulk_g2s(&S.row[0][0], rowtab + blk<inv::R>(lc, r0, L), ns * inv::R * 16, &sm.full[b]);
+        bulk_g2s(&S.colc[0][0], a.colc + oc, ns * inv::C * 8, &sm.full[b]);
+        bulk_g2s(&S.gp[0][0], gp + oc, ns * inv::C * 16, &sm.full[b]);
+        if (!REAL) bulk_g2s(&S.gn[0][0], gn + oc, ns * inv::C * 16, &sm.full[b]);
       }
     }
     return;

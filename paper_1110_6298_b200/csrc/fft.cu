@@ -394,9 +394,9 @@ __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
       }
       v = cscale(v, inv);
       if (neg && (j & 1)) v = make_double2(-v.x, -v.y);
-      gT[(long long)j * ldw + am] = v;
+      gT[blk<kTileCols>(j, am, L)] = v;
       if (!REAL && m == 0)
-        gT[(long long)L * ldw + (long long)j * ldw] = (j & 1) ? make_double2(-v.x, -v.y) : v;
+        gT[(long long)L * ldw + blk<kTileCols>(j, 0, L)] = (j & 1) ? make_double2(-v.x, -v.y) : v;
     }
     team_sync<C::TEAM>(team);
   }

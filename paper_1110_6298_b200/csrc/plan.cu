@@ -62,8 +62,8 @@ static int fail(int code, const char* what, const char* detail) {
 
 
 struct SpinTab {
-  double2* rowinv = nullptr;  // [l*ldw + m'] = (kap_l C_l(m'), W_l(m'))
-  double2* rowfwd = nullptr;  // [m'*ldw + l] = (alpha(l-m'+1) beta(l+m'-1), W'(l, m'))
+  double2* rowinv = nullptr;  // [blk64(l, m')] = (kap_l C_l(m'), W_l(m'))
+  double2* rowfwd = nullptr;  // [blk64(m', l)] = (alpha(l-m'+1) beta(l+m'-1), W'(l, m'))
 };
 
 struct mwsht_plan {
@@ -92,7 +92,7 @@ struct mwsht_plan {
   int own_launches = 0;
   bool timing = false;
   cudaEvent_t ev[2][3] = {};  // [forward|inverse][start, core start, core end]
-  double* colc = nullptr;  // [l*ldw + m] = C_l(m)
+  double* colc = nullptr;  // [blk32(l, m)] = C_l(m)
   std::vector<long double> hl_A, hl_V, hl_Bt, hl_lam, hl_kap;  // host tables for the spin builds
   std::mutex mu;
 };
@@ -219,7 +219,8 @@ static int build_tables(mwsht_plan* p) {
   std::vector<double> colc((size_t)L * Lp, 0.0);
   host_parallel(L, [&](int lo, int hi) {
     for (int l = lo; l < hi; l++)
-      for (int m = 0; m <= l; m++) colc[(size_t)l * Lp + m] = (double)((ld)m * V[l - m] * V[l + m]);
+      for (int m = 0; m <= l; m++)
+        colc[blk<kTileCols>(l, m, L)] = (double)((ld)m * V[l - m] * V[l + m]);
   });
   if ((rc = upload(p, &p->colc, colc))) return rc;
   return MWSHT_OK;
@@ -229,8 +230,8 @@ static int build_tables(mwsht_plan* p) {
 // the Trapani column recursion (_numba.py:63-71) run in 80-bit long double
 // (whose exponent range removes the reference's float64 overflow), and is
 // packed with the recursion coefficients each core reads per step:
-//   rowinv[l*ldw + x] = (kap_l C_l(x),               (-1)^l lam_l u_l(x) Delta^l_{x,-s})
-//   rowfwd[x*ldw + l] = (alpha(l-x+1) beta(l+x-1),   A(l-x) Bt(l+x) Delta^l_{x,-s})
+//   rowinv[blk64(l, x)] = (kap_l C_l(x),             (-1)^l lam_l u_l(x) Delta^l_{x,-s})
+//   rowfwd[blk64(x, l)] = (alpha(l-x+1) beta(l+x-1), A(l-x) Bt(l+x) Delta^l_{x,-s})
 // with C_l(x) = x V(l-x) V(l+x), u_l(x) = A(l-x) A(l+x)  (common.cuh).
 static int build_spin(mwsht_plan* p, int spin) {
   if (p->spins.count(spin)) return MWSHT_OK;
@@ -267,13 +268,13 @@ static int build_spin(mwsht_plan* p, int spin) {
         ld wi = lam[l] * A[l - x] * A[l + x] * dv;
         if (l & 1) wi = -wi;
         const ld cx = kap[l] * (ld)x * V[l - x] * V[l + x];
-        inv[(size_t)l * Lp + x] = make_double2((double)cx, (double)wi);
+        inv[blk<kTileRows>(l, x, L)] = make_double2((double)cx, (double)wi);
         ld qn = 0.0L;
         if (x >= 1) {
           const int pp = l - x + 1, qq = l + x - 1;
           qn = (2.0L * A[pp - 1] / (A[pp] * sq[pp])) * (Bt[qq + 1] / (Bt[qq] * sq[qq + 1]));
         }
-        fwd[(size_t)x * Lp + l] = make_double2((double)qn, (double)(A[l - x] * Bt[l + x] * dv));
+        fwd[blk<kTileRows>(x, l, L)] = make_double2((double)qn, (double)(A[l - x] * Bt[l + x] * dv));
       }
     }
   });

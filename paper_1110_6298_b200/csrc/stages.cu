@@ -85,7 +85,7 @@ __global__ void k_mul_spectrum(double2* __restrict__ C, const double2* __restric
 //   gf[r][j] = G_r(j) + s_r G_r(-j)  (j = m' >= 0; gf[r][0] = G_r(0)), G_r(m') = C[r][3L-3+m'],
 //   s_r = (-1)^(m+s) (complex, m = r-(L-1)) or (-1)^r (real),
 // written transposed and split by the sign of m, zero-padded to ldw columns:
-//   gfT[j][m] = gf[row(+m)][j],  gfT[L*ldw + j*ldw + m] = (-1)^j gf[row(-m)][j].
+//   gfT[blk32(j, m)] = gf[row(+m)][j],  gfT[L*ldw + blk32(j, m)] = (-1)^j gf[row(-m)][j].
 // SRC_CONV: read G from the correlation rows C (length P); else read an
 // already folded (rows x L) plane (kernel-level hook input).
 template <bool REAL, bool SRC_CONV>
@@ -123,7 +123,7 @@ __global__ void k_fold_T2(const double2* __restrict__ src, double2* __restrict__
   __syncthreads();
   for (int k = ty; k < 32; k += 8) {
     const int j = jb + k, m = mb + tx;
-    if (j < L && m < ldw) g[(long long)j * ldw + m] = tile[tx][k];
+    if (j < L && m < ldw) g[blk<kTileCols>(j, m, L)] = tile[tx][k];
   }
 }
 
@@ -140,7 +140,7 @@ __global__ void k_T2_to_fold(const double2* __restrict__ gfT, double2* __restric
     const int j = jb + k, m = mb + tx;
     double2 v = make_double2(0.0, 0.0);
     if (j < L && m < L) {
-      v = g[(long long)j * ldw + m];
+      v = g[blk<kTileCols>(j, m, L)];
       if (neg && (j & 1)) v = make_double2(-v.x, -v.y);
     }
     tile[k][tx] = v;
@@ -157,7 +157,7 @@ __global__ void k_T2_to_fold(const double2* __restrict__ gfT, double2* __restric
 
 // Inverse: coefficients -> the core's pre-scaled staging rows (mw.py:390-392
 // unflatten + the c_l u_l(m) column factor of the l-recursion):
-//   gp[l*ldw+m] = c_l u_l(m) f_{l,m},  gn[l*ldw+m] = (-1)^l c_l u_l(m) f_{l,-m},
+//   gp[blk32(l, m)] = c_l u_l(m) f_{l,m},  gn[blk32(l, m)] = (-1)^l c_l u_l(m) f_{l,-m},
 //   u_l(m) = A(l-m) A(l+m), zero for m > l.
 // in_mode 0: flat l(l+1)+m; 1: table (L, N) column L-1+m (real: (L, L) column m).
 template <bool REAL>
@@ -188,8 +188,8 @@ __global__ void k_inv_prescale(const double2* __restrict__ in, int in_mode,
       vp = cscale(fp, u);
       vn = cscale(fn, (l & 1) ? -u : u);
     }
-    p[(long long)l * ldw + m] = vp;
-    if (!REAL) n[(long long)l * ldw + m] = vn;
+    p[blk<kTileCols>(l, m, L)] = vp;
+    if (!REAL) n[blk<kTileCols>(l, m, L)] = vn;
   }
 }
 
