@@ -103,7 +103,7 @@ constexpr int kConsumerRegs = 232;
 constexpr int kTileRows = 64;  // inverse: m' rows; forward: l rows
 constexpr int kTileCols = 32;  // m columns
 constexpr int kChunk = 16;     // l (inverse) or m' (forward) steps per pipeline stage
-constexpr int kStages = 4;     // depth of the mbarrier ring
+constexpr int kStages = 5;     // depth of the mbarrier ring
 
 // All 2-D plan tables and staged planes have leading dimension ldw = L rounded
 // up to kTileRows, zero-padded, so every bulk copy is in bounds and aligned.
