@@ -168,6 +168,16 @@ __device__ __forceinline__ void team_sync(int team) {
     asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(TEAM) : "memory");
 }
 
+// Storage order of the precomputed spectra: the fused innermost pass (radix R,
+// butterfly b = lt + q*TEAM reads positions b*R + k) finds its R values at
+// (q*R + k)*TEAM + lt, so each warp-wide load is one contiguous 512-byte run
+// instead of 32 lines 128 bytes apart.  Natural order when a team has idle
+// lanes (H/R < TEAM).
+template <int H, int R, int TEAM>
+__host__ __device__ constexpr int spec_index(int b, int k, int lt) {
+  return ((H / R) % TEAM == 0) ? (b - lt) * R + k * TEAM + lt : b * R + k;
+}
+
 // One radix-R pass on sub-length n (stride s = n/R), compile-time shape.  MODE:
 //   0 DIF   (load via LD, butterfly, twiddle, store via ST)
 //   1 DIT   (load, untwiddle, inverse butterfly, store)
@@ -198,9 +208,10 @@ __device__ __forceinline__ void pass(const double2* tw, const double2* spec, int
 #pragma unroll
       for (int r = 0; r < R; r++) st(base + r * s, x[r]);
     } else {
+      // spectra are stored thread-major (spec_index): a warp's loads coalesce
       double2 sp[R];
 #pragma unroll
-      for (int k = 0; k < R; k++) sp[k] = spec[base + k];
+      for (int k = 0; k < R; k++) sp[k] = spec[spec_index<H, R, TEAM>(b, k, lt)];
 #pragma unroll
       for (int r = 0; r < R; r++) x[r] = ld(base + r);
       net_fwd<R>(x);
@@ -484,7 +495,11 @@ __global__ void __launch_bounds__(kT, 1) k_spectrum(FftArgs a, const double2* ke
     }
     team_sync<C::TEAM>(0);
     dif_all<LOGH, 0>(tws, lt, lds, sts);
-    for (int j = lt; j < C::H; j += C::TEAM) spec[half * C::H + j] = X[phys(j)];
+    constexpr int RL = 1 << C::lr(C::NP - 1);
+    for (int j = lt; j < C::H; j += C::TEAM) {
+      const int b = j / RL, k = j - b * RL;
+      spec[half * C::H + spec_index<C::H, RL, C::TEAM>(b, k, b % C::TEAM)] = X[phys(j)];
+    }
     team_sync<C::TEAM>(0);
   }
 }
