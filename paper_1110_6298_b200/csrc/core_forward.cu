@@ -295,9 +295,29 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
             }
         };
         auto run = [&](auto masked) {
-          if (SPIN0) {
-            // contraction when m' has the warp's degree parity
-            const bool first_full = ((mc & 1) == par);
+          // contraction when m' has the warp's degree parity (spin 0)
+          const bool first_full = ((mc & 1) == par);
+          if (ns == kChunk) {
+            // full chunk: straight-line code, compile-time smem offsets
+            if (SPIN0) {
+              if (first_full) {
+#pragma unroll
+                for (int s = 0; s < kChunk; s += 2) {
+                  full_step(masked, s);
+                  rec_step(s + 1);
+                }
+              } else {
+#pragma unroll
+                for (int s = 0; s < kChunk; s += 2) {
+                  rec_step(s);
+                  full_step(masked, s + 1);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int s = 0; s < kChunk; s++) full_step(masked, s);
+            }
+          } else if (SPIN0) {
             int s = 0;
             for (; s + 1 < ns; s += 2) {
               if (first_full) {
@@ -315,7 +335,6 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
                 rec_step(s);
             }
           } else {
-#pragma unroll 2
             for (int s = 0; s < ns; s++) full_step(masked, s);
           }
         };

@@ -303,10 +303,29 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
             }
         };
         auto run = [&](auto masked) {
-          if (SPIN0) {
-            // lc is even (tile corners are multiples of 32): pairs (even l, odd l)
+          if (ns == kChunk) {
+            // full chunk: straight-line code, compile-time smem offsets
+            if (SPIN0) {
+              // lc is even (tile corners are multiples of 32): pairs (even l, odd l)
+              if (par == 0) {
+#pragma unroll
+                for (int s = 0; s < kChunk; s += 2) {
+                  full_step(masked, s);
+                  rec_step(s + 1);
+                }
+              } else {
+#pragma unroll
+                for (int s = 0; s < kChunk; s += 2) {
+                  rec_step(s);
+                  full_step(masked, s + 1);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int s = 0; s < kChunk; s++) full_step(masked, s);
+            }
+          } else if (SPIN0) {
             int s = 0;
-#pragma unroll 2
             for (; s + 1 < ns; s += 2) {
               if (par == 0) {
                 full_step(masked, s);
@@ -323,7 +342,6 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
                 rec_step(s);
             }
           } else {
-#pragma unroll 2
             for (int s = 0; s < ns; s++) full_step(masked, s);
           }
         };
