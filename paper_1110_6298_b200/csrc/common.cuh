@@ -90,13 +90,11 @@ __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_dou
 // ---------------------------------------------------------------- core args
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumerThreads = 32 * kConsumerWarps;
-constexpr int kCoreThreads = kConsumerThreads + 32;  // forward core: + one TMA producer warp
-// Inverse core CTA = 3 warpgroups: warpgroup 0 holds the TMA producer warp
-// (its other three warps retire) and gives up registers with setmaxnreg;
-// warpgroups 1-2 are the 8 consumer warps, which raise their budget to
-// kConsumerRegs (per SMSP: 40 + 2 x 232 regs/thread x 32 <= 64 KB).  The
-// forward core measured slower this way (10.4 -> 11.4 ms at L=4096) and keeps
-// the 288-thread layout capped at 168 registers.
+// Core CTA = 3 warpgroups: warpgroup 0 holds the TMA producer warp (its other
+// three warps retire) and gives up registers with setmaxnreg; warpgroups 1-2
+// are the 8 consumer warps, which raise their budget to kConsumerRegs (per
+// SMSP: 40 + 2 x 232 regs/thread x 32 lanes <= 64 KB).  With a single
+// 288-thread layout the consumers were capped at 168 registers.
 constexpr int kCoreThreadsWS = 128 + kConsumerThreads;
 constexpr int kProducerRegs = 40;
 constexpr int kConsumerRegs = 232;

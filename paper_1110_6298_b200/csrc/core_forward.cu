@@ -13,10 +13,12 @@
 //
 // CTA: 8 consumer warps own 64 degrees l x 32 orders m, 4x2 chains per thread;
 // a warp's 16 degrees share one parity (spin 0: Delta^l_{m',0} = 0 when l-m'
-// is odd, so whole warps skip alternate contraction steps).  A 9th warp
-// streams, per 16-value chunk of m' (walking down), the plan-table rows
-// (coefficient, W'(l, m')) and the transposed folded plane rows gfT[m'][+m]
-// and (-1)^m' gfT[m'][-m] with TMA bulk copies into a 4-stage mbarrier ring.
+// is odd, so whole warps skip alternate contraction steps).  A producer warp
+// (warpgroup 0, registers handed to the consumers with setmaxnreg) streams,
+// per 16-value chunk of m' (walking down), the plan-table rows (coefficient,
+// W'(l, m')) and the folded staging rows gfT[m'][+m] and (-1)^m' gfT[m'][-m]
+// with one TMA bulk copy per array into a kStages-deep mbarrier ring (the
+// tables and staging planes are column-blocked, common.cuh).
 #include "common.cuh"
 
 namespace mwsht {
@@ -49,16 +51,10 @@ __device__ __forceinline__ void rescale(double (&y)[NE], double (&y1)[NE], unsig
   }
 }
 
-// Spin 0 keeps the 288-thread layout (one producer warp, 168-register cap);
-// spin != 0 runs the warp-specialised 384-thread layout (see common.cuh),
-// which measured faster for it (13.7 -> 13.3 ms at L=4096) and slower for
-// spin 0 (10.4 -> 11.4 ms).
-template <bool SPIN0>
-constexpr int fwd_threads() { return SPIN0 ? kCoreThreads : kCoreThreadsWS; }
-
+// Warp-specialised 384-thread CTA (common.cuh): warpgroup 0 = TMA producer,
+// warpgroups 1-2 = 8 consumer warps with a raised register budget.
 template <bool REAL, bool SPIN0>
-__global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArgs a) {
-  constexpr bool WS = !SPIN0;
+__global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
   constexpr int NI = 4, NJ = 2, NE = NI * NJ;
   constexpr int NG = REAL ? 1 : 2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -81,11 +77,10 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
   }
   __syncthreads();
 
-  if (WS ? wall < 4 : wall == kConsumerWarps) {
-    if (WS) {
-      setmaxnreg_dec<kProducerRegs>();
-      if (wall != 0) return;
-    }
+  if (wall < 4) {
+    // warpgroup 0: warp 0 streams the stages, warps 1-3 retire
+    setmaxnreg_dec<kProducerRegs>();
+    if (wall != 0) return;
     // ------------------------------------------------------------ producer
     const double2* gp = a.gf + (long long)blockIdx.y * a.in_stride;
     const double2* gn = gp + (long long)L * Lp;
@@ -111,8 +106,8 @@ __global__ void __launch_bounds__(fwd_threads<SPIN0>(), 1) k_forward_core(FwdArg
   }
 
   // -------------------------------------------------------------- consumers
-  if (WS) setmaxnreg_inc<kConsumerRegs>();
-  const int w = WS ? wall - 4 : wall, tid = WS ? threadIdx.x - 128 : threadIdx.x;
+  setmaxnreg_inc<kConsumerRegs>();
+  const int w = wall - 4, tid = threadIdx.x - 128;
   double2* __restrict__ out = a.out + (long long)blockIdx.y * a.out_stride;
   const int wr = w & 3, wc = w >> 2, r = lane & 3, c = lane >> 2, par = wr & 1;
   int rl[NI], cl[NJ], ll[NI], mm[NJ];
@@ -406,7 +401,7 @@ static void launch_fwd(const FwdArgs& a, dim3 grid, cudaStream_t st) {
   const size_t smem = sizeof(fwd::Smem);
   cudaFuncSetAttribute(k_forward_core<REAL, SPIN0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  k_forward_core<REAL, SPIN0><<<grid, fwd_threads<SPIN0>(), smem, st>>>(a);
+  k_forward_core<REAL, SPIN0><<<grid, kCoreThreadsWS, smem, st>>>(a);
 }
 
 void launch_forward_core(const FwdArgs& a, int ntiles, int nmaps, bool real, cudaStream_t st) {

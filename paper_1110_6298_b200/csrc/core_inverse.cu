@@ -10,13 +10,15 @@
 //
 // CTA: 8 consumer warps own a 64 (m') x 32 (m) tile, 4x2 chains per thread;
 // a warp's 16 rows share one parity (spin 0: Delta^l_{m',0} = 0 when l+m' is
-// odd, so a whole warp skips the contraction on alternate degrees).  A 9th
-// warp is the producer: it streams the per-degree parameters -- rows of the
-// plan table (kap_l C_l(m'), W_l(m')), rows of C_l(m), and rows of the
-// pre-scaled coefficients c_l u_l(m) f_{l,+-m} -- with TMA bulk copies
-// (cp.async.bulk -> UBLKCP) into a 4-deep ring of 16-degree stages guarded by
-// full/empty mbarriers (one bulk copy per array and stage: the tables and
-// staging planes are column-blocked, common.cuh).  Consumer warps never meet at a CTA barrier.
+// odd, so a whole warp skips the contraction on alternate degrees).  A
+// producer warp (warpgroup 0, registers handed to the consumers with
+// setmaxnreg) streams the per-degree parameters -- rows of the plan table
+// (kap_l C_l(m'), W_l(m')), rows of C_l(m), and rows of the pre-scaled
+// coefficients c_l u_l(m) f_{l,+-m} -- with TMA bulk copies (cp.async.bulk ->
+// UBLKCP) into a kStages-deep ring of 16-degree stages guarded by full/empty
+// mbarriers, one bulk copy per array and stage (the tables and staging planes
+// are column-blocked, common.cuh).  Consumer warps never meet at a CTA barrier;
+// full 16-degree chunks run as straight-line code.
 #include "common.cuh"
 
 namespace mwsht {
