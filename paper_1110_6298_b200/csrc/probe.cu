@@ -7,17 +7,18 @@
 
 namespace {
 // 16 independent chains per thread, 32 warps per SM; one fresh register operand
-// per DFMA (the multiplier and addend are shared), so the register file never
-// limits the issue rate (tools/fp64_micro.cu: three distinct operands reach
-// only ~23 TF/s).
+// per DFMA (shared multiplier, immediate addend), so the register file never
+// limits the issue rate and the DFMA pipe's own peak is measured
+// (tools/fp64_micro.cu: a register addend caps it near 34 TF/s, three distinct
+// register operands near 23 TF/s).
 constexpr int kChains = 16;
-__global__ void __launch_bounds__(512) k_dfma(double* out, int iters, double a, double b) {
+__global__ void __launch_bounds__(512) k_dfma(double* out, int iters, double a) {
   double x[kChains];
 #pragma unroll
   for (int k = 0; k < kChains; k++) x[k] = threadIdx.x * 1e-3 + k;
   for (int i = 0; i < iters; i++) {
 #pragma unroll
-    for (int k = 0; k < kChains; k++) x[k] = fma(x[k], a, b);
+    for (int k = 0; k < kChains; k++) x[k] = fma(x[k], a, 1e-9);
   }
   double s = 0;
 #pragma unroll
@@ -32,15 +33,15 @@ extern "C" int mwsht_fp64_probe(int device, double* tflops, double* ms) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   double* out;
   if (cudaMalloc(&out, 8) != cudaSuccess) return MWSHT_E_NOMEM;
-  const int blocks = sms * 2, threads = 512, iters = 4096;
+  const int blocks = sms * 2, threads = 512, iters = 32768;  // ~4 ms
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  k_dfma<<<blocks, threads>>>(out, 64, 0.999999, 1e-7);  // warm-up
+  k_dfma<<<blocks, threads>>>(out, 64, 0.999999);  // warm-up
   float best = 1e30f;
   for (int rep = 0; rep < 5; rep++) {
     cudaEventRecord(e0);
-    k_dfma<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+    k_dfma<<<blocks, threads>>>(out, iters, 0.999999);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float t;
