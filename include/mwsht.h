@@ -171,6 +171,14 @@ int mwsht_shard_inverse_front(mwsht_plan *plan, const void *flm, int m0, int m1,
 int mwsht_shard_inverse_phi(mwsht_plan *plan, const void *OUT, int t0, int t1, void *samples_rows,
                             void *stream);
 
+/* Inverse-core tiling (no reference counterpart; a scheduling choice only).
+ * Paired tiles: each (m', m) chain with m' > m also produces the transposed
+ * output T[m, m'] (Delta^l_{m m'} = (-1)^(m'-m) Delta^l_{m' m}), so one
+ * recursion feeds two contractions.  Spin 0 only.  mode 0: plain tiles
+ * everywhere; mode 1 or -1 (default): paired tiles for spin 0.  Results
+ * agree to rounding (tests/test_gpu_paired.py). */
+int mwsht_plan_set_paired(mwsht_plan *plan, int mode);
+
 /* Per-call event timing of the O(L^3) core kernel (bench / roofline).  When
  * enabled, each transform records CUDA events on its stream around the FFT
  * stages and around the core kernel; last_timing synchronises on them. */

@@ -54,6 +54,7 @@ _SIGS = {
     "mwsht_forward_stages_z": ([_P, _P, _P, _I, _P], _I),
     "mwsht_plan_last_launches": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
     "mwsht_plan_set_timing": ([_P, _I], _I),
+    "mwsht_plan_set_paired": ([_P, _I], _I),
     "mwsht_shard_forward_phi": ([_P, _P, _I, _I, _P, _P], _I),
     "mwsht_shard_forward_rest": ([_P, _P, _I, _I, _I, _P, _P], _I),
     "mwsht_shard_inverse_front": ([_P, _P, _I, _I, _I, _P, _P], _I),

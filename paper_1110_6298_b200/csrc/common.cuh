@@ -113,9 +113,11 @@ struct InvArgs {
                           // gn = gp + L*ldw: c_l u_l(m) (-1)^l f_{l,-m}  (zero for m > l)
   double2* out;           // out_mode 0: theta-synthesis spectrum (N,N) [complex] / (L,N) [real]
                           // out_mode 1: raw T (L,N) [complex] / (L,L) [real]
+  const double* wcol;     // paired tiles: [blk32(l, m)] = W_l(m) (the row weight at column indices)
   const int2* tiles;
   int out_mode, spin;
   int ldw;
+  int paired;                      // tiles cover the lower triangle and also emit the transpose
   long long g_stride, out_stride;  // per-map element strides (batch = gridDim.y)
 };
 

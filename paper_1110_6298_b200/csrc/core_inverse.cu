@@ -19,6 +19,9 @@
 // mbarriers, one bulk copy per array and stage (the tables and staging planes
 // are column-blocked, common.cuh).  Consumer warps never meet at a CTA barrier;
 // full 16-degree chunks run as straight-line code.
+//
+// Spin 0 uses the paired variant of this kernel (core_inverse_paired.cu),
+// which feeds two contractions from one recursion via the transpose symmetry.
 #include "common.cuh"
 
 namespace mwsht {
@@ -424,7 +427,14 @@ static void launch_inv(const InvArgs& a, dim3 grid, cudaStream_t st) {
   k_inverse_core<REAL, SPIN0><<<grid, kCoreThreadsWS, smem, st>>>(a);
 }
 
+void launch_inverse_core_paired(const InvArgs& a, int ntiles, int nmaps, bool real,
+                                cudaStream_t st);  // core_inverse_paired.cu
+
 void launch_inverse_core(const InvArgs& a, int ntiles, int nmaps, bool real, cudaStream_t st) {
+  if (a.paired) {
+    launch_inverse_core_paired(a, ntiles, nmaps, real, st);
+    return;
+  }
   dim3 grid(ntiles, nmaps);
   if (real)
     launch_inv<true, true>(a, grid, st);

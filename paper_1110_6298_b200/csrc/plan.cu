@@ -64,6 +64,7 @@ static int fail(int code, const char* what, const char* detail) {
 struct SpinTab {
   double2* rowinv = nullptr;  // [blk64(l, m')] = (kap_l C_l(m'), W_l(m'))
   double2* rowfwd = nullptr;  // [blk64(m', l)] = (alpha(l-m'+1) beta(l+m'-1), W'(l, m'))
+  double* wcol = nullptr;     // [blk32(l, x)] = W_l(x) (paired inverse tiles)
 };
 
 struct mwsht_plan {
@@ -73,8 +74,9 @@ struct mwsht_plan {
   std::vector<void*> allocs;
   size_t bytes = 0;
   std::map<int, SpinTab> spins;
-  int2 *tiles_inv = nullptr, *tiles_fwd = nullptr;
-  int ntiles_inv = 0, ntiles_fwd = 0;
+  int2 *tiles_inv = nullptr, *tiles_fwd = nullptr, *tiles_invp = nullptr;
+  int ntiles_inv = 0, ntiles_fwd = 0, ntiles_invp = 0;
+  int paired_mode = -1;  // inverse core: -1 auto (paired tiles for spin 0), 0 off, 1 on
   struct TileSet {
     int2 *inv = nullptr, *fwd = nullptr;
     int ninv = 0, nfwd = 0;
@@ -239,6 +241,7 @@ static int build_spin(mwsht_plan* p, int spin) {
   const int L = p->L, cs = spin < 0 ? -spin : spin;
   const int Lp = p->ldw;
   std::vector<double2> inv((size_t)L * Lp, make_double2(0.0, 0.0)), fwd(inv);
+  std::vector<double> wcol((size_t)L * Lp, 0.0);
   std::vector<ld> sq(2 * L + 4);
   for (size_t i = 0; i < sq.size(); i++) sq[i] = sqrtl((ld)i);
   std::vector<ld> t0sq(L);
@@ -269,6 +272,7 @@ static int build_spin(mwsht_plan* p, int spin) {
         if (l & 1) wi = -wi;
         const ld cx = kap[l] * (ld)x * V[l - x] * V[l + x];
         inv[blk<kTileRows>(l, x, L)] = make_double2((double)cx, (double)wi);
+        wcol[blk<kTileCols>(l, x, L)] = (double)wi;
         ld qn = 0.0L;
         if (x >= 1) {
           const int pp = l - x + 1, qq = l + x - 1;
@@ -282,6 +286,7 @@ static int build_spin(mwsht_plan* p, int spin) {
   int rc;
   if ((rc = upload(p, &st.rowinv, inv))) return rc;
   if ((rc = upload(p, &st.rowfwd, fwd))) return rc;
+  if ((rc = upload(p, &st.wcol, wcol))) return rc;
   p->spins[spin] = st;
   return MWSHT_OK;
 }
@@ -292,24 +297,36 @@ static int build_tiles(mwsht_plan* p) {
     int2 t;
     long long w;
   };
-  std::vector<Tl> inv, fwd;
+  std::vector<Tl> inv, fwd, invp;
   for (int r0 = 0; r0 < L; r0 += kTileRows)
     for (int c0 = 0; c0 < L; c0 += kTileCols)
       inv.push_back({make_int2(r0, c0), (long long)(L - std::max(r0, c0))});
+  // paired: tiles with c0 <= r0 + 32.  32x32 blocks strictly below the
+  // diagonal also produce their transpose (weight ~1.6x: the recursion is
+  // shared), diagonal blocks run plain, blocks above the diagonal are idle.
+  for (int r0 = 0; r0 < L; r0 += kTileRows)
+    for (int c0 = 0; c0 < L && c0 <= r0 + kTileCols; c0 += kTileCols) {
+      const long long len = L - std::max(r0, c0);
+      invp.push_back({make_int2(r0, c0), c0 + kTileCols <= r0 ? (len * 8) / 5 : len});
+    }
   for (int l0 = 0; l0 < L; l0 += kTileRows) {
     const int top = std::min(l0 + kTileRows - 1, L - 1);
     for (int c0 = 0; c0 <= top; c0 += kTileCols) fwd.push_back({make_int2(l0, c0), (long long)top + 1});
   }
   auto by_work = [](const Tl& a, const Tl& b) { return a.w > b.w; };
   std::stable_sort(inv.begin(), inv.end(), by_work);
+  std::stable_sort(invp.begin(), invp.end(), by_work);
   std::stable_sort(fwd.begin(), fwd.end(), by_work);
-  std::vector<int2> hi, hf;
+  std::vector<int2> hi, hf, hp;
   for (auto& x : inv) hi.push_back(x.t);
+  for (auto& x : invp) hp.push_back(x.t);
   for (auto& x : fwd) hf.push_back(x.t);
   int rc;
   if ((rc = upload(p, &p->tiles_inv, hi))) return rc;
+  if ((rc = upload(p, &p->tiles_invp, hp))) return rc;
   if ((rc = upload(p, &p->tiles_fwd, hf))) return rc;
   p->ntiles_inv = (int)hi.size();
+  p->ntiles_invp = (int)hp.size();
   p->ntiles_fwd = (int)hf.size();
   return MWSHT_OK;
 }
@@ -475,17 +492,32 @@ static int check_spin(mwsht_plan* p, int spin) {
 }
 
 // ------------------------------------------------------------ pipelines
+// Paired inverse tiles (core_inverse_paired.cu) cover the lower triangle
+// m' > m and emit the transposed outputs from the same chains.  Built for
+// spin 0 (complex and real), where they measured 4-11% faster than the plain
+// tiles at L = 1024-4096; spin != 0 runs the plain kernel (the paired
+// variant's extra shared-memory traffic made it slower there).
+static bool use_paired(const mwsht_plan* p, int spin) {
+  return spin == 0 && p->paired_mode != 0;
+}
+
 static InvArgs inv_args(mwsht_plan* p, int spin) {
   InvArgs a{};
   a.t = p->tabs;
   a.rowtab = p->spins[spin].rowinv;
+  a.wcol = p->spins[spin].wcol;
   a.colc = p->colc;
   a.gp = p->bufG;
   a.g_stride = p->strideG;
-  a.tiles = p->tiles_inv;
+  a.paired = use_paired(p, spin) ? 1 : 0;
+  a.tiles = a.paired ? p->tiles_invp : p->tiles_inv;
   a.spin = spin;
   a.ldw = p->ldw;
   return a;
+}
+
+static int inv_ntiles(const mwsht_plan* p, const InvArgs& a) {
+  return a.paired ? p->ntiles_invp : p->ntiles_inv;
 }
 
 static FwdArgs fwd_args(mwsht_plan* p, int spin) {
@@ -578,7 +610,7 @@ static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int
   a.out = p->bufB;
   a.out_mode = 0;
   a.out_stride = (long long)rows * N;
-  launch_inverse_core(a, p->ntiles_inv, nm, real, st);
+  launch_inverse_core(a, inv_ntiles(p, a), nm, real, st);
   LAUNCHED(p);
   if (p->timing) CU(cudaEventRecord(p->ev[1][2], st));
   // 2. theta synthesis (mw.py:441-446), keep t < L, transposed to rings (:436-437)
@@ -768,7 +800,7 @@ int mwsht_fmm_core(mwsht_plan* p, const void* flm2d, const double* cl, int spin,
   InvArgs a = inv_args(p, spin);
   a.out = (double2*)T;
   a.out_mode = 1;
-  launch_inverse_core(a, p->ntiles_inv, 1, false, st);
+  launch_inverse_core(a, inv_ntiles(p, a), 1, false, st);
   LAUNCHED(p);
   return MWSHT_OK;
 }
@@ -787,7 +819,7 @@ int mwsht_fmm_core_real(mwsht_plan* p, const void* flm_half, const double* cl, i
   InvArgs a = inv_args(p, 0);
   a.out = (double2*)T;
   a.out_mode = 1;
-  launch_inverse_core(a, p->ntiles_inv, 1, true, st);
+  launch_inverse_core(a, inv_ntiles(p, a), 1, true, st);
   LAUNCHED(p);
   return MWSHT_OK;
 }
@@ -918,6 +950,7 @@ int mwsht_shard_inverse_front(mwsht_plan* p, const void* flm, int m0, int m1, in
                       (long long)L * L, p->strideG, 1, st);
   LAUNCHED(p);
   InvArgs a = inv_args(p, spin);
+  a.paired = 0;  // order-restricted tiles: the transpose would leave the shard's orders
   a.tiles = ts->inv;
   a.out = p->bufB;
   a.out_mode = 0;
@@ -955,6 +988,15 @@ int mwsht_shard_inverse_phi(mwsht_plan* p, const void* OUT, int t0, int t1, void
   f.out_stride = 0;
   fft_launch(3, false, f, p->nsm, (cudaStream_t)stream);
   LAUNCHED(p);
+  return MWSHT_OK;
+}
+
+int mwsht_plan_set_paired(mwsht_plan* p, int mode) {
+  int rc;
+  if ((rc = check_plan(p))) return rc;
+  if (mode < -1 || mode > 1) return fail(MWSHT_E_VALUE, "paired", "mode must be -1, 0 or 1");
+  std::lock_guard<std::mutex> lk(p->mu);
+  p->paired_mode = mode;
   return MWSHT_OK;
 }
 

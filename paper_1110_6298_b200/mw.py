@@ -159,6 +159,11 @@ class Plan:
                                              _lib.ctypes.byref(cf))
         return own.value, cf.value
 
+    def set_paired(self, mode):
+        """Inverse-core tiling for spin 0: 1 or -1 (default) paired tiles (one
+        recursion feeds T[m',m] and its transpose), 0 plain tiles."""
+        _lib.call("mwsht_plan_set_paired", self.handle, int(mode))
+
     def prepare_spin(self, spin):
         _lib.call("mwsht_plan_prepare_spin", self.handle, int(spin))
 

@@ -19,10 +19,12 @@ ap.add_argument("--L", type=int, default=2048)
 ap.add_argument("--spin", type=int, default=0)
 ap.add_argument("--real", action="store_true")
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--paired", type=int, default=-1)
 a = ap.parse_args()
 L, s = a.L, a.spin
 v = gaussian_real_coeffs(L, 0) if a.real else gaussian_coeffs(L, s, 0)
 f = torch.from_numpy(v).cuda()
+mw.get_plan(L).set_paired(a.paired)
 for _ in range(a.reps):
     if a.real:
         sig = mw.inverse_real(mw.HarmonicCoeffs(L, 0, f))

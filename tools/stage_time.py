@@ -20,10 +20,12 @@ ap.add_argument("--L", type=int, default=4096)
 ap.add_argument("--spin", type=int, default=0)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--real", action="store_true")
+ap.add_argument("--paired", type=int, default=-1)
 a = ap.parse_args()
 L, s = a.L, a.spin
 lib = _lib.load()
 plan = mw.get_plan(L, 0)
+plan.set_paired(a.paired)
 lib.mwsht_plan_set_timing(plan.handle, 1)
 from oracle.mw_oracle import gaussian_real_coeffs  # noqa: E402
 f = torch.from_numpy(gaussian_real_coeffs(L, 0) if a.real else gaussian_coeffs(L, s, 0)).cuda()
@@ -54,6 +56,6 @@ for r in range(a.reps + 1):
         rows.append((e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), inv_core, c.value, g.value))
 m = np.median(np.array(rows), axis=0)
 err = float((back - f).abs().max())
-print(f"{os.environ.get('MWSHT_LIB', 'in-tree')}: inverse {m[0]:.2f} ms (core {m[2]:.2f}, stages "
+print(f"L={L} s={s} real={a.real} paired={a.paired} {os.environ.get('MWSHT_LIB', 'in-tree')}: inverse {m[0]:.2f} ms (core {m[2]:.2f}, stages "
       f"{m[0]-m[2]:.2f}) | forward {m[1]:.2f} ms (stages {m[4]:.2f}, core {m[3]:.2f}) | "
       f"pair {m[0]+m[1]:.2f} ms | err {err:.1e}")
