@@ -329,23 +329,42 @@ __device__ __forceinline__ void bluestein(double2* X, const double2* tw, double2
 
 // phi DFT of each ring (forward): AT[k][t] = (2 pi/N) sum_p f[t][p] e^{-2 pi i kp/N}
 // complex: k < N, AT is (N, L); real: k < L (rfft bins), AT is (L, L).
+// Real rings go two per transform: z = f_t + i f_{t+1}, Z = DFT_N(z), then
+// F_t[k] = (Z[k] + conj Z[N-k]) / 2 and F_{t+1}[k] = (Z[k] - conj Z[N-k]) / 2i.
 template <bool REAL, int LOGH>
 __global__ void __launch_bounds__(kT, 1) k_phi_fwd(FftArgs a) {
   FFT_PROLOGUE
   const int L = a.L, N = a.N;
   const int kout = REAL ? L : N;
   const double sc = 2.0 * 3.141592653589793 / (double)N / (double)C::M;
-  for (int row = blockIdx.x * C::NR + team; row < a.nrows * a.nmaps; row += gridDim.x * C::NR) {
-    const int map = row / a.nrows, tl = row - map * a.nrows, t = a.t0 + tl;
+  const int per_map = REAL ? (a.nrows + 1) / 2 : a.nrows;  // transforms per map
+  for (int row = blockIdx.x * C::NR + team; row < per_map * a.nmaps; row += gridDim.x * C::NR) {
+    const int map = row / per_map, q = row - map * per_map;
     double2* at = (double2*)a.out + (long long)map * a.out_stride;
-    auto fin = [&](int k, double2 y) {
-      if (k < kout) at[(long long)k * L + t] = cscale(cmulc(y, a.chirp[k]), sc);
-    };
     if (REAL) {
+      const int tl = 2 * q, t = a.t0 + tl;
+      const bool two = tl + 1 < a.nrows;
       const double* f = (const double*)a.in + (long long)map * a.in_stride + (long long)tl * N;
-      bluestein<LOGH, false>(X, tws, scr, a, lt, team,
-                             [&](int n) { return make_double2(f[n], 0.0); }, fin);
+      const double* f2 = two ? f + N : f;
+      bluestein<LOGH, false>(
+          X, tws, scr, a, lt, team,
+          [&](int n) { return make_double2(f[n], two ? f2[n] : 0.0); },
+          [&](int k, double2 y) {
+            if (k < N) X[phys(k)] = cmulc(y, a.chirp[k]);
+          });
+      team_sync<C::TEAM>(team);
+      const double h = 0.5 * sc;
+      for (int k = lt; k < L; k += C::TEAM) {
+        const double2 zk = X[phys(k)], zn = X[phys(k ? N - k : 0)];
+        at[(long long)k * L + t] = make_double2(h * (zk.x + zn.x), h * (zk.y - zn.y));
+        if (two) at[(long long)k * L + t + 1] = make_double2(h * (zk.y + zn.y), h * (zn.x - zk.x));
+      }
+      team_sync<C::TEAM>(team);
     } else {
+      const int tl = q, t = a.t0 + tl;
+      auto fin = [&](int k, double2 y) {
+        if (k < kout) at[(long long)k * L + t] = cscale(cmulc(y, a.chirp[k]), sc);
+      };
       const double2* f = (const double2*)a.in + (long long)map * a.in_stride + (long long)tl * N;
       bluestein<LOGH, false>(X, tws, scr, a, lt, team, [&](int n) { return f[n]; }, fin);
     }
@@ -441,22 +460,38 @@ __global__ void __launch_bounds__(kT, 1) k_theta_inv(FftArgs a) {
 
 // inverse phi synthesis per ring t: samples[t][p] = sum_m Out[t][bin(m)] e^{+2 pi i m p/N}
 // (real: Hermitian completion of the m >= 0 half, real part out; mw.py:558).
+// Real rings go two per transform: IDFT(X_t + i X_{t+1}) = x_t + i x_{t+1}.
 template <bool REAL, int LOGH>
 __global__ void __launch_bounds__(kT, 1) k_phi_inv(FftArgs a) {
   FFT_PROLOGUE
   const int L = a.L, N = a.N;
   const double inv = 1.0 / (double)C::M;
-  for (int row = blockIdx.x * C::NR + team; row < a.nrows * a.nmaps; row += gridDim.x * C::NR) {
-    const int map = row / a.nrows, tl = row - map * a.nrows, t = a.t0 + tl;
+  const int per_map = REAL ? (a.nrows + 1) / 2 : a.nrows;  // transforms per map
+  for (int row = blockIdx.x * C::NR + team; row < per_map * a.nmaps; row += gridDim.x * C::NR) {
+    const int map = row / per_map, q = row - map * per_map;
     if (REAL) {
+      const int tl = 2 * q, t = a.t0 + tl;
+      const bool two = tl + 1 < a.nrows;
       const double2* h = (const double2*)a.in + (long long)map * a.in_stride + (long long)t * L;
+      const double2* h2 = h + L;
       double* o = (double*)a.out + (long long)map * a.out_stride + (long long)tl * N;
       bluestein<LOGH, true>(
-          X, tws, scr, a, lt, team, [&](int n) { return n < L ? h[n] : conjd(h[N - n]); },
+          X, tws, scr, a, lt, team,
+          [&](int n) {
+            const double2 x1 = n < L ? h[n] : conjd(h[N - n]);
+            if (!two) return x1;
+            const double2 x2 = n < L ? h2[n] : conjd(h2[N - n]);
+            return make_double2(x1.x - x2.y, x1.y + x2.x);  // x1 + i x2
+          },
           [&](int p, double2 y) {
-            if (p < N) o[p] = cmul(y, a.chirp[p]).x * inv;
+            if (p < N) {
+              const double2 v = cmul(y, a.chirp[p]);
+              o[p] = v.x * inv;
+              if (two) o[N + p] = v.y * inv;
+            }
           });
     } else {
+      const int tl = q, t = a.t0 + tl;
       const double2* h = (const double2*)a.in + (long long)map * a.in_stride + (long long)t * N;
       double2* o = (double2*)a.out + (long long)map * a.out_stride + (long long)tl * N;
       bluestein<LOGH, true>(X, tws, scr, a, lt, team, [&](int n) { return h[n]; },
