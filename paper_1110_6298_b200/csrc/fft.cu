@@ -185,7 +185,9 @@ __host__ __device__ constexpr int spec_index(int b, int k, int lt) {
 template <int R, int MODE, int H, int M, int n, int TEAM, class LD, class ST>
 __device__ __forceinline__ void pass(const double2* tw, const double2* spec, int lt, LD ld, ST st) {
   constexpr int s = n / R, nb = H / R, tstep = M / n;
-#pragma unroll 2
+  // one butterfly per thread when nb == TEAM (H = 8192): no unrolled copy (code size)
+  constexpr int UNR = nb > TEAM ? 2 : 1;
+#pragma unroll UNR
   for (int b = lt; b < nb; b += TEAM) {
     const int blk = b / s, j = b - blk * s, base = blk * n + j;
     double2 x[R];
@@ -371,6 +373,37 @@ __global__ void __launch_bounds__(kT, 1) k_phi_fwd(FftArgs a) {
   }
 }
 
+// Inverse theta rows go two per Bluestein transform.  Row m's synthesis
+// output is a reflection about t = L-1 with sign eps_m = (-1)^(m+s)
+// (F_{m,-m'} = eps_m F_{m,m'}, mw.py:400-401), and consecutive orders m, m+1
+// have opposite signs, so the transform of S_1 + i S_2 separates exactly:
+// z = y_1 + i y_2 and eps_1 z[N-1-t] = y_1[t] - i y_2[t].
+// (The forward stage keeps one row per transform: pairing it measured slower,
+// its kernel outgrew the instruction cache.)
+// Tasks pair the orders of magnitude 2k and 2k+1 within the +m block and
+// within the -m block, so a sharded order range [m0, m1) with even bounds
+// pairs exactly as the whole plane does (bit-identical shards).
+__device__ __forceinline__ int pair_count(int lo, int hi) {  // k with [2k, 2k+1] meeting [lo, hi)
+  return hi > lo ? (hi - 1) / 2 - lo / 2 + 1 : 0;
+}
+__device__ __forceinline__ int theta_tasks(int m0, int m1, bool real) {
+  return pair_count(m0, m1) + (real ? 0 : pair_count(m0 > 0 ? m0 : 1, m1));
+}
+// rows of task q: i1 and, when it returns 2, i1 + 1 (row_order indexing)
+__device__ __forceinline__ int theta_task(int q, int m0, int m1, bool real, int& i1) {
+  const int tp = pair_count(m0, m1);
+  int lo = m0, off = 0;
+  if (!real && q >= tp) {
+    q -= tp;
+    lo = m0 > 0 ? m0 : 1;
+    off = m1 - m0;
+  }
+  const int k = lo / 2 + q;
+  const int first = max(2 * k, lo), last = min(2 * k + 1, m1 - 1);
+  i1 = off + (first - lo);
+  return last - first + 1;
+}
+
 // theta stage of the forward transform for each order row (m from row_order):
 // extension (mw.py:161-177), DFT_N + twist (:180-192), weight correlation
 // (:244-251) and m' fold (:273-285, 504-511), written in the forward core's
@@ -440,21 +473,46 @@ __global__ void __launch_bounds__(kT, 1) k_theta_inv(FftArgs a) {
   const int L = a.L, N = a.N;
   const int ocols = REAL ? L : N;
   const double inv = 1.0 / (double)C::M;
-  for (int row = blockIdx.x * C::NR + team; row < a.nrows * a.nmaps; row += gridDim.x * C::NR) {
-    const int map = row / a.nrows, i = row - map * a.nrows;
-    const int m = row_order(i, a.m0, a.m1, REAL);
-    const int r = REAL ? m : m + (L - 1);  // plane row of order m
-    const double2* s = (const double2*)a.in + (long long)map * a.in_stride + (long long)r * N;
+  const int ntask = theta_tasks(a.m0, a.m1, REAL);
+  for (int task = blockIdx.x * C::NR + team; task < ntask * a.nmaps; task += gridDim.x * C::NR) {
+    const int map = task / ntask, q = task - map * ntask;
+    int i1;
+    const bool two = theta_task(q, a.m0, a.m1, REAL, i1) == 2;
+    int mr[2], col[2];
+    const double2* sp[2];
+    for (int u = 0; u < 2; u++) {
+      mr[u] = row_order(two ? i1 + u : i1, a.m0, a.m1, REAL);
+      const int r = REAL ? mr[u] : mr[u] + (L - 1);  // plane row of order m
+      sp[u] = (const double2*)a.in + (long long)map * a.in_stride + (long long)r * N;
+      col[u] = REAL ? mr[u] : fbin(mr[u], N);
+    }
+    const double e1 = (((mr[0] + (REAL ? 0 : a.spin)) & 1) ? -1.0 : 1.0);
     double2* o = (double2*)a.out + (long long)map * a.out_stride;
-    const int col = REAL ? m : fbin(m, N);
-    bluestein<LOGH, true>(X, tws, scr, a, lt, team, [&](int n) { return s[n]; },
-                          [&](int t, double2 y) {
-                            if (t < L) {
-                              double2 v = cscale(cmul(y, a.chirp[t]), inv);
-                              if (REAL && m == 0) v.y = 0.0;  // irfft ignores Im of the DC bin
-                              o[(long long)t * ocols + col] = v;
-                            }
-                          });
+    bluestein<LOGH, true>(
+        X, tws, scr, a, lt, team,
+        [&](int n) {
+          const double2 s1 = sp[0][n];
+          if (!two) return s1;
+          const double2 s2 = sp[1][n];
+          return make_double2(s1.x - s2.y, s1.y + s2.x);  // S_1 + i S_2
+        },
+        [&](int t, double2 y) {
+          if (t < N) X[phys(t)] = cscale(cmul(y, a.chirp[t]), inv);
+        });
+    team_sync<C::TEAM>(team);
+    for (int t = lt; t < L; t += C::TEAM) {
+      const double2 z = X[phys(t)];
+      double2 v1 = z;
+      if (two) {
+        const double2 zr = cscale(X[phys(N - 1 - t)], e1);
+        v1 = cscale(cadd(z, zr), 0.5);
+        const double2 w = csub(z, zr);  // 2i y_2
+        o[(long long)t * ocols + col[1]] = make_double2(0.5 * w.y, -0.5 * w.x);
+      }
+      if (REAL && mr[0] == 0) v1.y = 0.0;  // irfft ignores Im of the DC bin
+      o[(long long)t * ocols + col[0]] = v1;
+    }
+    team_sync<C::TEAM>(team);
   }
 }
 

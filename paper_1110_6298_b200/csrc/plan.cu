@@ -615,6 +615,7 @@ static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int
   if (p->timing) CU(cudaEventRecord(p->ev[1][2], st));
   // 2. theta synthesis (mw.py:441-446), keep t < L, transposed to rings (:436-437)
   fft::FftArgs f = fft_args(p);
+  f.spin = spin;
   f.nmaps = nm;
   f.nrows = rows;
   f.in = p->bufB;
@@ -960,6 +961,7 @@ int mwsht_shard_inverse_front(mwsht_plan* p, const void* flm, int m0, int m1, in
     LAUNCHED(p);
   }
   fft::FftArgs f = fft_args(p);
+  f.spin = spin;
   f.m0 = m0;
   f.m1 = m1;
   f.nrows = 2 * (m1 - m0) - (m0 == 0 ? 1 : 0);
