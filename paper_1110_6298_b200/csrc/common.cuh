@@ -31,8 +31,16 @@ struct DevTables {
   const double* lam;    // [L+2]
   const double* kap;    // [L+2]
   const double* cl;     // [L]   sqrt((2l+1)/4pi), as numpy computes it (mw.py:144-146)
-  const double* seed_mant;  // triangle n(n+1)/2+k : mantissa of sqrt(C(2n,n+k))/2^n
-  const int* seed_exp;      //                      : binary exponent
+  // Chain seeds as products of 1-D factors, each (mantissa in [0.5,1), binary
+  // exponent) because the factorials leave every floating range:
+  //   inverse z^{l0} = +-Pi(l0) Qi(l0+mu) Qi(l0-mu),  l0 = max(m',m), mu = min(m',m)
+  //   forward y_l    = +-Pf(l)  R(l+m)   R(l-m)
+  // R(j) = 1/sqrt(j!), Qi(j) = R(j)/A(j), P0(n) = sqrt((2n)!)/2^n,
+  // Pi(n) = P0(n)/(lam_n A(2n)), Pf(n) = P0(n)/Bt(2n)  (plan.cu build_tables).
+  const double2* sd_pi;  // [L]
+  const double2* sd_qi;  // [2L]
+  const double2* sd_pf;  // [L]
+  const double2* sd_r;   // [2L]
 };
 
 // Exponent-level machinery.  A chain whose true value is
@@ -68,10 +76,10 @@ __device__ __forceinline__ bool above_top(double z) {
   return (__double2hiint(z) & 0x7ff00000) >= ((1023 + kLevTop) << 20);
 }
 
-__device__ __forceinline__ double seed_value(const DevTables& t, int n, int k, int& ex) {
-  long long idx = (long long)n * (n + 1) / 2 + k;
-  ex = t.seed_exp[idx];
-  return t.seed_mant[idx];
+// product of three (mantissa, exponent) factors: returns the mantissa product, ex = exponent sum
+__device__ __forceinline__ double seed3(double2 a, double2 b, double2 c, int& ex) {
+  ex = (int)a.y + (int)b.y + (int)c.y;
+  return a.x * b.x * c.x;
 }
 
 // i^p for p mod 4, as (re, im)

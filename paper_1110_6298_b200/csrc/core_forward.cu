@@ -138,9 +138,9 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
       int lev = 0;
       if (mm[j] <= ll[i] && ll[i] < L) {
         int ex;
-        double s_ = seed_value(T, ll[i], mm[j], ex);
+        double s_ = seed3(T.sd_pf[ll[i]], T.sd_r[ll[i] + mm[j]], T.sd_r[ll[i] - mm[j]], ex);
         if ((ll[i] - mm[j]) & 1) s_ = -s_;
-        ys = split_level(s_ / T.Bt[2 * ll[i]], ex, lev);
+        ys = split_level(s_, ex, lev);
       }
       sm.seedy[e][tid] = ys;
       slv |= (unsigned)lev << (4 * e);

@@ -26,6 +26,10 @@
 
 namespace mwsht {
 
+#ifdef MWSHT_PROF_WAIT
+__device__ unsigned long long g_prof[8];
+#endif
+
 namespace inv {
 constexpr int R = kTileRows, C = kTileCols, CH = kChunk, NB = kStages;
 struct Stage {
@@ -107,6 +111,10 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
 
   // -------------------------------------------------------------- consumers
   setmaxnreg_inc<kConsumerRegs>();
+#ifdef MWSHT_PROF_WAIT
+  const long long t_start = clock64();
+  long long t_wait = 0, t_first = 0;
+#endif
   const int w = wall - 4, tid = threadIdx.x - 128;
   double2* __restrict__ out = a.out + (long long)blockIdx.y * a.out_stride;
   const int wr = w & 3, wc = w >> 2, r = lane & 3, c = lane >> 2, par = wr & 1;
@@ -126,7 +134,8 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
   asm volatile("" : "+r"(rl0), "+r"(cl0));
 
   // seeds: z^{l0} = Delta^{l0}_{m'm} / ((-1)^l0 lam_l0 u_l0(m) u_l0(m')), l0 = max(m', m),
-  // Delta^{l0}_{m'm} = sign sqrt(C(2 l0, l0 + min))/2^l0, carried in exponent levels
+  // Delta^{l0}_{m'm} = sign sqrt(C(2 l0, l0 + min))/2^l0 = sign P0(l0) R(l0+mu) R(l0-mu)
+  // (common.cuh seed factors), carried in exponent levels
   unsigned slv = 0;  // seed levels, 4 bits per chain
 #pragma unroll
   for (int i = 0; i < NI; i++)
@@ -136,19 +145,21 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
       double zs = 0.0;
       int lev = 0;
       if (mp[i] < L && mm[j] < L) {
-        const int l0 = max(mp[i], mm[j]);
+        const int l0 = max(mp[i], mm[j]), mu = min(mp[i], mm[j]);
         int ex;
-        double s_ = seed_value(T, l0, min(mp[i], mm[j]), ex);
+        double s_ = seed3(T.sd_pi[l0], T.sd_qi[l0 + mu], T.sd_qi[l0 - mu], ex);
         if (mm[j] < mp[i] && ((mp[i] - mm[j]) & 1)) s_ = -s_;
-        double den = T.lam[l0] * (T.A[l0 - mm[j]] * T.A[l0 + mm[j]]) *
-                     (T.A[l0 - mp[i]] * T.A[l0 + mp[i]]);
-        if (l0 & 1) den = -den;
-        zs = split_level(s_ / den, ex, lev);
+        if (l0 & 1) s_ = -s_;
+        zs = split_level(s_, ex, lev);
       }
       sm.seedz[e][tid] = zs;
       slv |= (unsigned)lev << (4 * e);
     }
 
+#ifdef MWSHT_PROF_WAIT
+  const long long t_seeded = clock64();
+  long long t_ramp = 0;
+#endif
   double z[NE], zp[NE], acc[NE][2 * NG];
 #pragma unroll
   for (int e = 0; e < NE; e++) {
@@ -170,7 +181,15 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
 
   for (int k = 0; k < nchunks; k++) {
     const int b = k % inv::NB, lc = lstart + k * kChunk, ns = min(kChunk, L - lc);
+#ifdef MWSHT_PROF_WAIT
+    const long long tw0 = clock64();
+#endif
     mbar_wait(&sm.full[b], (k / inv::NB) & 1);
+#ifdef MWSHT_PROF_WAIT
+    bool is_ramp = false;
+    long long tr0 = 0;
+    if (k == 0) t_first += clock64() - tw0; else t_wait += clock64() - tw0;
+#endif
     // rl[i] = rl0 + 8 i, cl[j] = cl0 + 8 j: one base pointer per array and chunk,
     // constant offsets per entry (rl0/cl0 opaque: never rematerialised from %tid)
     const inv::Stage& S = sm.st[b];
@@ -181,6 +200,10 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
 
     if (warp_has && wl0_min < lc + ns) {
       if (!fast) fast = (wl0_max < lc) && __all_sync(0xffffffffu, lv == 0);
+#ifdef MWSHT_PROF_WAIT
+      tr0 = clock64();
+      is_ramp = !fast && wl0_max >= lc;
+#endif
       if (!fast && wl0_max >= lc) {
         // --------------------------------- ramp: seed injection, levels, masking
         // Chains not yet started are exactly 0 and contribute nothing; chains
@@ -361,10 +384,23 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
         }
       }
     }
+#ifdef MWSHT_PROF_WAIT
+    if (is_ramp) t_ramp += clock64() - tr0;
+#endif
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[b]);
   }
 
+#ifdef MWSHT_PROF_WAIT
+  if (lane == 0) {
+    atomicAdd(&g_prof[0], (unsigned long long)t_wait);
+    atomicAdd(&g_prof[1], (unsigned long long)(clock64() - t_start));
+    atomicAdd(&g_prof[2], (unsigned long long)t_first);
+    atomicAdd(&g_prof[3], 1ull);
+    atomicAdd(&g_prof[4], (unsigned long long)(t_seeded - t_start));
+    atomicAdd(&g_prof[5], (unsigned long long)t_ramp);
+  }
+#endif
   // ---------------------------------------------------------------- epilogue
   const int sgs = (a.spin & 1) ? -1 : 1;  // (-1)^s
 #pragma unroll
@@ -444,4 +480,17 @@ void launch_inverse_core(const InvArgs& a, int ntiles, int nmaps, bool real, cud
     launch_inv<false, false>(a, grid, st);
 }
 
+#ifdef MWSHT_PROF_WAIT
 }  // namespace mwsht
+extern "C" int mwsht_debug_prof(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, mwsht::g_prof, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(mwsht::g_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#else
+}  // namespace mwsht
+#endif

@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
   asm volatile("" : "+r"(rl0), "+r"(cl0), "+r"(hr0));
 
   // seeds: z^{l0} = Delta^{l0}_{m'm} / ((-1)^l0 lam_l0 u_l0(m) u_l0(m')), l0 = max(m', m),
-  // Delta^{l0}_{m'm} = sign sqrt(C(2 l0, l0 + min))/2^l0, carried in exponent levels
+  // Delta^{l0}_{m'm} = sign sqrt(C(2 l0, l0 + min))/2^l0 = sign P0(l0) R(l0+mu) R(l0-mu)
+  // (common.cuh seed factors), carried in exponent levels
   unsigned slv = 0;  // seed levels, 4 bits per chain
 #pragma unroll
   for (int i = 0; i < NI; i++)
@@ -165,14 +166,12 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
       double zs = 0.0;
       int lev = 0;
       if (mp[i] < L && mm[j] < L) {
-        const int l0 = max(mp[i], mm[j]);
+        const int l0 = max(mp[i], mm[j]), mu = min(mp[i], mm[j]);
         int ex;
-        double s_ = seed_value(T, l0, min(mp[i], mm[j]), ex);
+        double s_ = seed3(T.sd_pi[l0], T.sd_qi[l0 + mu], T.sd_qi[l0 - mu], ex);
         if (mm[j] < mp[i] && ((mp[i] - mm[j]) & 1)) s_ = -s_;
-        double den = T.lam[l0] * (T.A[l0 - mm[j]] * T.A[l0 + mm[j]]) *
-                     (T.A[l0 - mp[i]] * T.A[l0 + mp[i]]);
-        if (l0 & 1) den = -den;
-        zs = split_level(s_ / den, ex, lev);
+        if (l0 & 1) s_ = -s_;
+        zs = split_level(s_, ex, lev);
       }
       sm.seedz[e][tid] = zs;
       slv |= (unsigned)lev << (4 * e);

@@ -165,26 +165,35 @@ static int build_tables(mwsht_plan* p) {
   }
   for (int l = 0; l < L; l++) hcl[l] = sqrt((2.0 * l + 1.0) / (4.0 * 3.141592653589793));
 
-  // top-row seeds T(n, k) = sqrt(C(2n, n+k)) / 2^n, 0 <= k <= n < L
-  const size_t ntri = (size_t)L * (L + 1) / 2;
-  std::vector<double> smant(ntri);
-  std::vector<int> sexp(ntri);
-  std::vector<ld> t0sq(L);
-  t0sq[0] = 1.0L;
-  for (int j = 1; j < L; j++) t0sq[j] = t0sq[j - 1] * (ld)(2 * j - 1) / (ld)(2 * j);
-  host_parallel(L, [&](int lo, int hi) {
-    for (int n = lo; n < hi; n++) {
-      ld P = t0sq[n];
-      const size_t base = (size_t)n * (n + 1) / 2;
-      for (int k = 0; k <= n; k++) {
-        int e;
-        ld f = frexpl(sqrtl(P), &e);
-        smant[base + k] = (double)f;
-        sexp[base + k] = e;
-        if (k < n) P = P * (ld)(n - k) / (ld)(n + k + 1);
-      }
-    }
-  });
+  // chain-seed factors (common.cuh DevTables): values as (long double mantissa,
+  // exponent) pairs renormalised every step, rounded once to (double, exponent)
+  struct XL {
+    ld m;
+    long e;
+  };
+  auto norm = [](XL x) {
+    int e;
+    x.m = frexpl(x.m, &e);
+    x.e += e;
+    return x;
+  };
+  auto mul = [&](XL a, XL b) { return norm(XL{a.m * b.m, a.e + b.e}); };
+  auto inv = [&](XL a) { return norm(XL{1.0L / a.m, -a.e}); };
+  auto dev = [](XL x) { return make_double2((double)x.m, (double)x.e); };
+  const int J = 2 * L + 2;
+  std::vector<XL> R(J);
+  R[0] = XL{0.5L, 1};
+  for (int j = 1; j < J; j++) R[j] = norm(XL{R[j - 1].m / sqrtl((ld)j), R[j - 1].e});
+  std::vector<double2> hpi(L), hqi(J), hpf(L), hr(J);
+  for (int j = 0; j < J; j++) {
+    hr[j] = dev(R[j]);
+    hqi[j] = dev(mul(R[j], inv(norm(XL{A[j], 0}))));
+  }
+  for (int n = 0; n < L; n++) {
+    const XL P0 = inv(norm(XL{R[2 * n].m, R[2 * n].e + n}));  // sqrt((2n)!) / 2^n
+    hpi[n] = dev(mul(P0, inv(norm(XL{lam[n] * A[2 * n], 0}))));
+    hpf[n] = dev(mul(P0, inv(norm(XL{Bt[2 * n], 0}))));
+  }
   int rc;
   DevTables& T = p->tabs;
   T.L = L;
@@ -206,11 +215,15 @@ static int build_tables(mwsht_plan* p) {
   T.kap = d;
   if ((rc = upload(p, &d, hcl))) return rc;
   T.cl = d;
-  if ((rc = upload(p, &d, smant))) return rc;
-  T.seed_mant = d;
-  int* di;
-  if ((rc = upload(p, &di, sexp))) return rc;
-  T.seed_exp = di;
+  double2* d2;
+  if ((rc = upload(p, &d2, hpi))) return rc;
+  T.sd_pi = d2;
+  if ((rc = upload(p, &d2, hqi))) return rc;
+  T.sd_qi = d2;
+  if ((rc = upload(p, &d2, hpf))) return rc;
+  T.sd_pf = d2;
+  if ((rc = upload(p, &d2, hr))) return rc;
+  T.sd_r = d2;
   p->hl_A = A;
   p->hl_V = V;
   p->hl_Bt = Bt;
