@@ -161,8 +161,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
   const int wrow_hi = min(wrow_lo + 30, L - 1);
   const int wcol_lo = c0 + 16 * wc;
   const bool warp_has = wrow_lo < L && wcol_lo <= wrow_hi;
-  const int wl_min = max(wrow_lo, wcol_lo);  // every valid chain has started once m' < wl_min
-  bool fast = false;
+  bool fast = false, started = false;
 
   for (int k = 0; k < nchunks; k++) {
     const int b = k % fwd::NB, mc = mu_top - k * kChunk, ns = min(kChunk, mc + 1);
@@ -174,70 +173,32 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
     const double2* gnp = &S.gn[fwd::CH - 1][0] + cl0;
 
     if (warp_has && wrow_hi >= mc - ns + 1) {
-      if (!fast) fast = (mc < wl_min) && __all_sync(0xffffffffu, lv == 0);
-      if (!fast && mc >= wl_min) {
-        // ---------------------------- ramp: chains starting, levels, masking
-        // Chains not yet started are exactly 0; chains carrying exponent levels
-        // are masked via `live`, which changes only at a start or a rescale.
-        unsigned live = level_zero_mask<NE>(lv);
-        for (int s = 0; s < ns; s++) {
-          const int mu = mc - s;
-          double2 qp[NI];
+      if (!started) {
+        // Ghost start: above its first value m' = l the
+        // chain's coefficient m alpha(l-m'+1) beta(l+m'-1) is exactly 0 (the
+        // tables are zero for m' > l), so (y_l, y_{l+1}) = (seed, 0) has the
+        // exact continuation y_mu = (-1)^((mu-l)/2) seed for mu = l mod 2,
+        // else 0.  Starting every chain there at this chunk's top value needs
+        // no per-step injection; the ghost terms meet W'(l, mu) = 0.
 #pragma unroll
-          for (int i = 0; i < NI; i++) qp[i] = rowp[-s * fwd::R + 8 * i];
-          if (mu >= ll[0] && mu <= ll[NI - 1]) {
+        for (int i = 0; i < NI; i++)
 #pragma unroll
-            for (int i = 0; i < NI; i++)
-              if (mu == ll[i]) {  // chains start with y_{l+1} = 0
-#pragma unroll
-                for (int j = 0; j < NJ; j++) {
-                  const int e = i * NJ + j;
-                  y[e] = sm.seedy[e][tid];
-                  y1[e] = 0.0;
-                  lv |= slv & (15u << (4 * e));
-                }
-              }
-            live = level_zero_mask<NE>(lv);
+          for (int j = 0; j < NJ; j++) {
+            const int e = i * NJ + j;
+            const int d = mc - ll[i];  // >= 0: the first chunk holds the warp's top degree
+            const double sd = sm.seedy[e][tid];
+            const double g0 = ((d >> 1) & 1) ? -sd : sd;        // y_{mc}   (d even)
+            const double g1 = (((d + 1) >> 1) & 1) ? -sd : sd;  // y_{mc+1} (d odd)
+            y[e] = (d & 1) ? 0.0 : g0;
+            y1[e] = (d & 1) ? g1 : 0.0;
           }
-          if ((!SPIN0 || ((mu & 1) == par)) && mu <= wrow_hi) {
-            double2 g[NJ][NG];
-#pragma unroll
-            for (int j = 0; j < NJ; j++) {
-              g[j][0] = gpp[-s * fwd::C + 8 * j];
-              if (!REAL) g[j][NG - 1] = gnp[-s * fwd::C + 8 * j];
-            }
-#pragma unroll
-            for (int i = 0; i < NI; i++)
-#pragma unroll
-              for (int j = 0; j < NJ; j++) {
-                const int e = i * NJ + j;
-                if ((live >> e) & 1u) {
-                  const double t = y[e] * qp[i].y;
-#pragma unroll
-                  for (int k2 = 0; k2 < NG; k2++) {
-                    acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
-                    acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
-                  }
-                }
-              }
-          }
-#pragma unroll
-          for (int i = 0; i < NI; i++)
-#pragma unroll
-            for (int j = 0; j < NJ; j++) {
-              const int e = i * NJ + j;
-              const double yn = fma(md[j] * qp[i].x, y[e], -y1[e]);
-              y1[e] = y[e];
-              y[e] = yn;
-            }
-          if (lv && (s & 3) == 3) {
-            rescale(y, y1, lv);
-            live = level_zero_mask<NE>(lv);
-          }
-        }
-      } else {
+        lv = slv;
+        started = true;
+      }
+      if (!fast) fast = __all_sync(0xffffffffu, lv == 0);
+      {
         // ------------------------------------------------------- steady state
-        // Every chain has started.  Chains still carrying exponent levels are
+        // Every chain runs (ghost or live).  Chains still carrying exponent levels are
         // masked out of the contraction for the whole chunk and checked for a
         // rescale once at its end (no overflow: stored values stay far below
         // 2^1023 within 16 steps of 2^200; a chain reaching level 0 inside the

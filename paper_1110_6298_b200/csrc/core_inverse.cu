@@ -26,9 +26,6 @@
 
 namespace mwsht {
 
-#ifdef MWSHT_PROF_WAIT
-__device__ unsigned long long g_prof[8];
-#endif
 
 namespace inv {
 constexpr int R = kTileRows, C = kTileCols, CH = kChunk, NB = kStages;
@@ -111,10 +108,6 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
 
   // -------------------------------------------------------------- consumers
   setmaxnreg_inc<kConsumerRegs>();
-#ifdef MWSHT_PROF_WAIT
-  const long long t_start = clock64();
-  long long t_wait = 0, t_first = 0;
-#endif
   const int w = wall - 4, tid = threadIdx.x - 128;
   double2* __restrict__ out = a.out + (long long)blockIdx.y * a.out_stride;
   const int wr = w & 3, wc = w >> 2, r = lane & 3, c = lane >> 2, par = wr & 1;
@@ -156,10 +149,6 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
       slv |= (unsigned)lev << (4 * e);
     }
 
-#ifdef MWSHT_PROF_WAIT
-  const long long t_seeded = clock64();
-  long long t_ramp = 0;
-#endif
   double z[NE], zp[NE], acc[NE][2 * NG];
 #pragma unroll
   for (int e = 0; e < NE; e++) {
@@ -171,25 +160,14 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
   unsigned lv = 0;  // current levels, 4 bits per chain (0 = true scale)
 
   const int wrow_lo = r0 + par + 32 * (wr >> 1);
-  const int wrow_hi = min(wrow_lo + 30, L - 1);
   const int wcol_lo = c0 + 16 * wc;
-  const int wcol_hi = min(wcol_lo + 15, L - 1);
   const bool warp_has = wrow_lo < L && wcol_lo < L;
   const int wl0_min = max(wrow_lo, wcol_lo);
-  const int wl0_max = max(wrow_hi, wcol_hi);
-  bool fast = false;
+  bool fast = false, started = false;
 
   for (int k = 0; k < nchunks; k++) {
     const int b = k % inv::NB, lc = lstart + k * kChunk, ns = min(kChunk, L - lc);
-#ifdef MWSHT_PROF_WAIT
-    const long long tw0 = clock64();
-#endif
     mbar_wait(&sm.full[b], (k / inv::NB) & 1);
-#ifdef MWSHT_PROF_WAIT
-    bool is_ramp = false;
-    long long tr0 = 0;
-    if (k == 0) t_first += clock64() - tw0; else t_wait += clock64() - tw0;
-#endif
     // rl[i] = rl0 + 8 i, cl[j] = cl0 + 8 j: one base pointer per array and chunk,
     // constant offsets per entry (rl0/cl0 opaque: never rematerialised from %tid)
     const inv::Stage& S = sm.st[b];
@@ -199,79 +177,34 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
     const double2* gnp = &S.gn[0][0] + cl0;
 
     if (warp_has && wl0_min < lc + ns) {
-      if (!fast) fast = (wl0_max < lc) && __all_sync(0xffffffffu, lv == 0);
-#ifdef MWSHT_PROF_WAIT
-      tr0 = clock64();
-      is_ramp = !fast && wl0_max >= lc;
-#endif
-      if (!fast && wl0_max >= lc) {
-        // --------------------------------- ramp: seed injection, levels, masking
-        // Chains not yet started are exactly 0 and contribute nothing; chains
-        // carrying exponent levels (true value below 2^-568) are masked via
-        // `live`, which changes only at an injection or a rescale.
-        const int tl0min = max(mp[0], mm[0]), tl0max = max(mp[NI - 1], mm[NJ - 1]);
-        unsigned live = level_zero_mask<NE>(lv);
-        for (int s = 0; s < ns; s++) {
-          const int l = lc + s;
-          double2 rp[NI];
-          double cc[NJ];
+      if (!started) {
+        // Ghost start: below its first degree l0 a chain's
+        // recursion coefficient kap_l C_l(m') C_l(m) is exactly 0 (the tables
+        // are zero for x > l), so the recursion maps (z^l, z^{l-1}) to
+        // (-z^{l-1}, z^l) and the pair (seed, 0) at l0 has the exact
+        // continuation z^l = (-1)^((l0-l)/2) seed for l = l0 mod 2, else 0.
+        // Starting every chain there at this chunk's first degree needs no
+        // per-degree injection; its ghost terms contract against W_l(m') or
+        // g_l(m), which are exactly 0 below l0.
 #pragma unroll
-          for (int i = 0; i < NI; i++) rp[i] = rowp[s * inv::R + 8 * i];
+        for (int i = 0; i < NI; i++)
 #pragma unroll
-          for (int j = 0; j < NJ; j++) cc[j] = colp[s * inv::C + 8 * j];
-          if (l >= tl0min && l <= tl0max) {
-#pragma unroll
-            for (int i = 0; i < NI; i++)
-#pragma unroll
-              for (int j = 0; j < NJ; j++) {
-                const int e = i * NJ + j;
-                if (l == max(mp[i], mm[j])) {  // chains start with z^{l0-1} = 0
-                  z[e] = sm.seedz[e][tid];
-                  zp[e] = 0.0;
-                  lv |= slv & (15u << (4 * e));
-                }
-              }
-            live = level_zero_mask<NE>(lv);
+          for (int j = 0; j < NJ; j++) {
+            const int e = i * NJ + j;
+            const int d = max(mp[i], mm[j]) - lc;  // >= 0: lc <= wl0_min <= l0
+            const double sd = (mp[i] < L && mm[j] < L) ? sm.seedz[e][tid] : 0.0;
+            const double g0 = ((d >> 1) & 1) ? -sd : sd;  // z^{lc}   (d even)
+            const double g1 = (((d + 1) >> 1) & 1) ? -sd : sd;  // z^{lc-1} (d odd)
+            z[e] = (d & 1) ? 0.0 : g0;
+            zp[e] = (d & 1) ? g1 : 0.0;
           }
-          if ((!SPIN0 || ((l & 1) == par)) && l >= wl0_min) {
-            double2 g[NJ][NG];
-#pragma unroll
-            for (int j = 0; j < NJ; j++) {
-              g[j][0] = gpp[s * inv::C + 8 * j];
-              if (!REAL) g[j][NG - 1] = gnp[s * inv::C + 8 * j];
-            }
-#pragma unroll
-            for (int i = 0; i < NI; i++)
-#pragma unroll
-              for (int j = 0; j < NJ; j++) {
-                const int e = i * NJ + j;
-                if ((live >> e) & 1u) {
-                  const double t = z[e] * rp[i].y;
-#pragma unroll
-                  for (int k2 = 0; k2 < NG; k2++) {
-                    acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
-                    acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
-                  }
-                }
-              }
-          }
-#pragma unroll
-          for (int i = 0; i < NI; i++)
-#pragma unroll
-            for (int j = 0; j < NJ; j++) {
-              const int e = i * NJ + j;
-              const double zn = fma(rp[i].x * cc[j], z[e], -zp[e]);
-              zp[e] = z[e];
-              z[e] = zn;
-            }
-          if (lv && (s & 3) == 3) {
-            rescale(z, zp, lv);
-            live = level_zero_mask<NE>(lv);
-          }
-        }
-      } else {
+        lv = slv;
+        started = true;
+      }
+      if (!fast) fast = __all_sync(0xffffffffu, lv == 0);
+      {
         // ------------------------------------------------------- steady state
-        // Every chain has started.  Chains still carrying exponent levels
+        // Every chain runs (ghost or live).  Chains still carrying exponent levels
         // (lv != 0: true value below 2^-568) are masked out of the contraction
         // for the whole chunk; one rescale check at the chunk end suffices
         // (a chain grows at most 4x per degree: 2^32 per chunk from <= 2^200),
@@ -384,23 +317,10 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
         }
       }
     }
-#ifdef MWSHT_PROF_WAIT
-    if (is_ramp) t_ramp += clock64() - tr0;
-#endif
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[b]);
   }
 
-#ifdef MWSHT_PROF_WAIT
-  if (lane == 0) {
-    atomicAdd(&g_prof[0], (unsigned long long)t_wait);
-    atomicAdd(&g_prof[1], (unsigned long long)(clock64() - t_start));
-    atomicAdd(&g_prof[2], (unsigned long long)t_first);
-    atomicAdd(&g_prof[3], 1ull);
-    atomicAdd(&g_prof[4], (unsigned long long)(t_seeded - t_start));
-    atomicAdd(&g_prof[5], (unsigned long long)t_ramp);
-  }
-#endif
   // ---------------------------------------------------------------- epilogue
   const int sgs = (a.spin & 1) ? -1 : 1;  // (-1)^s
 #pragma unroll
@@ -480,17 +400,5 @@ void launch_inverse_core(const InvArgs& a, int ntiles, int nmaps, bool real, cud
     launch_inv<false, false>(a, grid, st);
 }
 
-#ifdef MWSHT_PROF_WAIT
+
 }  // namespace mwsht
-extern "C" int mwsht_debug_prof(unsigned long long* out, int reset) {
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, mwsht::g_prof, sizeof(unsigned long long) * 8);
-  if (reset) {
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    cudaMemcpyToSymbol(mwsht::g_prof, z, sizeof(z));
-  }
-  return 0;
-}
-#else
-}  // namespace mwsht
-#endif

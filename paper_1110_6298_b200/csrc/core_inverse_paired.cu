@@ -192,9 +192,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
   unsigned lv = 0;  // current levels, 4 bits per chain (0 = true scale)
 
   const int wrow_lo = r0 + par + 32 * h;
-  const int wrow_hi = min(wrow_lo + 30, L - 1);
   const int wcol_lo = PAIRED ? c0 + pc : c0 + 16 * wc;
-  const int wcol_hi = min(wcol_lo + (PAIRED ? 30 : 15), L - 1);
   bool warp_has = wrow_lo < L && wcol_lo < L;
   bool mir = false;  // warp-uniform: this warp's block also emits the transpose
   if (PAIRED) {
@@ -203,8 +201,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
     mir = rb >= c0 + 32;
   }
   const int wl0_min = max(wrow_lo, wcol_lo);
-  const int wl0_max = max(wrow_hi, wcol_hi);
-  bool fast = false;
+  bool fast = false, started = false;
 
   for (int k = 0; k < nchunks; k++) {
     const int b = k % NB, lc = lstart + k * CH, ns = min(CH, L - lc);
@@ -279,101 +276,28 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
     };
 
     if (warp_has && wl0_min < lc + ns) {
-      if (!fast) fast = (wl0_max < lc) && __all_sync(0xffffffffu, lv == 0);
-      if (!fast && wl0_max >= lc) {
-        // --------------------------------- ramp: seed injection, levels, masking
-        // Chains not yet started are exactly 0 and contribute nothing; chains
-        // carrying exponent levels (true value below 2^-568) are masked via
-        // `live`, which changes only at an injection or a rescale.
-        const int tl0min = max(mp[0], mm[0]), tl0max = max(mp[NI - 1], mm[NJ - 1]);
-        unsigned live = level_zero_mask<NE>(lv);
-        for (int s = 0; s < ns; s++) {
-          const int l = lc + s;
-          if (l >= tl0min && l <= tl0max) {
+      if (!started) {
+        // Ghost start: see core_inverse.cu.  The transposed contraction's
+        // ghost terms meet W_l(m) or g_l(m'), likewise exactly 0 below l0.
 #pragma unroll
-            for (int i = 0; i < NI; i++)
+        for (int i = 0; i < NI; i++)
 #pragma unroll
-              for (int j = 0; j < NJ; j++) {
-                const int e = i * NJ + j;
-                if (l == max(mp[i], mm[j])) {  // chains start with z^{l0-1} = 0
-                  z[e] = sm.seedz[e][tid];
-                  zp[e] = 0.0;
-                  lv |= slv & (15u << (4 * e));
-                }
-              }
-            live = level_zero_mask<NE>(lv);
+          for (int j = 0; j < NJ; j++) {
+            const int e = i * NJ + j;
+            const int d = max(mp[i], mm[j]) - lc;  // >= 0: lc <= wl0_min <= l0
+            const double sd = (mp[i] < L && mm[j] < L) ? sm.seedz[e][tid] : 0.0;
+            const double g0 = ((d >> 1) & 1) ? -sd : sd;        // z^{lc}   (d even)
+            const double g1 = (((d + 1) >> 1) & 1) ? -sd : sd;  // z^{lc-1} (d odd)
+            z[e] = (d & 1) ? 0.0 : g0;
+            zp[e] = (d & 1) ? g1 : 0.0;
           }
-          const bool on = l >= wl0_min;
-          double2 rp[NI];
-          double cc[NJ];
-#pragma unroll
-          for (int i = 0; i < NI; i++) rp[i] = rowp[s * invp::R + 8 * i];
-#pragma unroll
-          for (int j = 0; j < NJ; j++) cc[j] = colp[s * invp::C + CJ * j];
-          if (on && (!SPIN0 || (l & 1) == par)) {
-            double2 g[NJ][NG];
-#pragma unroll
-            for (int j = 0; j < NJ; j++) {
-              g[j][0] = gpp[s * invp::C + CJ * j];
-              if (!REAL) g[j][NG - 1] = gnp[s * invp::C + CJ * j];
-            }
-#pragma unroll
-            for (int i = 0; i < NI; i++)
-#pragma unroll
-              for (int j = 0; j < NJ; j++) {
-                const int e = i * NJ + j;
-                if ((live >> e) & 1u) {
-                  const double t = z[e] * rp[i].y;
-#pragma unroll
-                  for (int k2 = 0; k2 < NG; k2++) {
-                    acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
-                    acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
-                  }
-                }
-              }
-          }
-          if (PAIRED && on && mir && (!SPIN0 || (l & 1) == pc)) {
-            double wv[NJ];
-            double2 gr[NI][NG];
-#pragma unroll
-            for (int j = 0; j < NJ; j++) wv[j] = wcp[s * invp::C + CJ * j];
-#pragma unroll
-            for (int i = 0; i < NI; i++) {
-              gr[i][0] = gprp[s * invp::C + 8 * i];
-              if (!REAL) gr[i][NG - 1] = gnrp[s * invp::C + 8 * i];
-            }
-#pragma unroll
-            for (int i = 0; i < NI; i++)
-#pragma unroll
-              for (int j = 0; j < NJ; j++) {
-                const int e = i * NJ + j;
-                if ((live >> e) & 1u) {
-                  const double t = z[e] * wv[j];
-#pragma unroll
-                  for (int k2 = 0; k2 < NG; k2++) {
-                    acm[e % NA][2 * k2] = fma(t, gr[i][k2].x, acm[e % NA][2 * k2]);
-                    acm[e % NA][2 * k2 + 1] = fma(t, gr[i][k2].y, acm[e % NA][2 * k2 + 1]);
-                  }
-                }
-              }
-          }
-#pragma unroll
-          for (int i = 0; i < NI; i++)
-#pragma unroll
-            for (int j = 0; j < NJ; j++) {
-              const int e = i * NJ + j;
-              const double zn = fma(rp[i].x * cc[j], z[e], -zp[e]);
-              zp[e] = z[e];
-              z[e] = zn;
-            }
-          if (lv && (s & 3) == 3) {
-            rescale_p(z, zp, lv);
-            live = level_zero_mask<NE>(lv);
-          }
-        }
-      } else {
+        lv = slv;
+        started = true;
+      }
+      if (!fast) fast = __all_sync(0xffffffffu, lv == 0);
+      {
         // ------------------------------------------------------- steady state
-        // Every chain has started.  Chains still carrying exponent levels
+        // Every chain runs (ghost or live).  Chains still carrying exponent levels
         // (lv != 0: true value below 2^-568) are masked out of the contraction
         // for the whole chunk; one rescale check at the chunk end suffices
         // (a chain grows at most 4x per degree: 2^32 per 16-degree chunk from <= 2^200),
