@@ -219,3 +219,46 @@ def test_basis_vectors_round_trip(mw):
                 values[ell * (ell + 1) + m] = 1.0
                 out = mw.forward(mw.inverse(mw.HarmonicCoeffs(L, spin, values)))
                 assert max_abs(out.values, values) < 1e-12, (ell, m)
+
+
+# ------------------------------------------------ large L (C4, C5 of BASELINE.json)
+
+def test_config4_L2048_matches_reference_risbo(mw, O):
+    # the reference's Trapani diverges above l ~ 1040; its Risbo
+    # carries ~1e-12 round-trip error at L = 2048, hence 2e-12
+    _cfg_check(mw, O, "L2048_s0_risbo", tol=2e-12)
+
+
+def test_config4_batch_of_8_maps(mw, O):
+    import torch
+    L, B = 2048, 8
+    vals = torch.from_numpy(np.stack([O.gaussian_coeffs(L, 0, k) for k in range(B)])).cuda()
+    sig = mw.inverse_batch(vals, L, 0)
+    back = mw.forward_batch(sig, L, 0)
+    assert (back - vals).abs().max().item() < 1e-11
+    g = golden_cfg("L2048_s0_risbo")   # map 0 = seed 0
+    s0 = sig[0].reshape(-1)[torch.from_numpy(g["samples_idx"]).cuda()].cpu().numpy()
+    assert max_abs(s0, g["samples_sub"]) / g["samples_checksums"][3] < 2e-12
+
+
+@pytest.mark.parametrize("spin", [0, 2])
+def test_config5_L4096_round_trip_and_linearity(mw, O, spin):
+    # C5: no reference output exists at this size (about an hour of CPU per
+    # transform); size-independent properties stand in: round trip (test_mw.py:44-53
+    # at 1e-12 scaled by L), linearity, and the l = 0 basis map (a constant).
+    import torch
+    L = 4096
+    v = torch.from_numpy(O.gaussian_coeffs(L, spin, 0)).cuda()
+    sig = mw.inverse(mw.HarmonicCoeffs(L, spin, v)).samples
+    back = mw.forward(mw.MwSignal(L, spin, sig)).values
+    err = (back - v).abs().max().item()
+    assert err < 1e-11, err
+    w = torch.from_numpy(O.gaussian_coeffs(L, spin, 1)).cuda()
+    sw = mw.inverse(mw.HarmonicCoeffs(L, spin, w)).samples
+    lin = mw.inverse(mw.HarmonicCoeffs(L, spin, 0.5 * v + w)).samples
+    assert (lin - (0.5 * sig + sw)).abs().max().item() < 1e-12 * sig.abs().max().item()
+    if spin == 0:
+        e0 = torch.zeros(L * L, dtype=torch.complex128, device="cuda")
+        e0[0] = 1.0
+        c = mw.inverse(mw.HarmonicCoeffs(L, 0, e0)).samples
+        assert (c - 1.0 / math.sqrt(4.0 * math.pi)).abs().max().item() < 1e-14
