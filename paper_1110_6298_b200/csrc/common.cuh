@@ -150,7 +150,10 @@ struct FftArgs {
   const double2* speci;   // inverse Bluestein spectrum (DFT_M of conj c)
   const double2* specw;   // weight-correlation spectrum (DFT_M of K'), 2pi included
   const double2* rho;     // forward theta glue: conj(c[k]) tau(f(k)) / M  (k < N)
-  double2* scratch;       // per-CTA L2 scratch: 2H complex per team
+  const double2* cen;     // paired forward theta rows: (-1)^k e^{i pi k/N}  (k < N)
+  const double2* wnk;     //                            e^{2 pi i k/N}       (k < N)
+  const double2* rho2;    //                            tau(f(k)) / (2 pi N M)
+  double2* scratch;       // per-CTA L2 scratch: 3H complex per team
   const void* in;         // stage input
   void* out;              // stage output
   long long in_stride, out_stride;  // per-map strides (elements)

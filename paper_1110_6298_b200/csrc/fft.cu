@@ -256,10 +256,40 @@ __device__ __forceinline__ void dit_chain(const double2* tw, int lt, int team, O
   }
 }
 
+template <int LOGH, int P, class LDS, class STS>
+__device__ __forceinline__ void dit_mid(const double2* tw, int lt, int team, LDS lds, STS sts) {
+  using C = Cfg<LOGH>;
+  if constexpr (P >= 1) {
+    constexpr int R = 1 << C::lr(P), n = C::n_at(P);
+    pass<R, 1, C::H, C::M, n, C::TEAM>(tw, nullptr, lt, lds, sts);
+    team_sync<C::TEAM>(team);
+    dit_mid<LOGH, P - 1>(tw, lt, team, lds, sts);
+  }
+}
+
+// The passes between the first DIF pass and the last DIT pass touch only the
+// shared-memory row, so call sites with OUTLINE share ONE out-of-line copy of
+// them: k_theta_fwd (four half-convolutions per task) then fits the
+// instruction cache, which its fully inlined form (7 passes per call site,
+// ~2.7k instructions each) did not.  Kernels with two call sites keep the
+// inlined form (the call costs ~3% there).
+template <int LOGH>
+__device__ __noinline__ void conv_middle(double2* X, const double2* tw, const double2* S, int lt,
+                                         int team) {
+  using C = Cfg<LOGH>;
+  auto lds = [&](int i) { return X[phys(i)]; };
+  auto sts = [&](int i, double2 v) { X[phys(i)] = v; };
+  constexpr int RL = 1 << C::lr(C::NP - 1), nL = C::n_at(C::NP - 1);
+  dif_chain<LOGH, 1>(tw, lt, team, lds, lds, sts);
+  pass<RL, 2, C::H, C::M, nL, C::TEAM>(tw, S, lt, lds, sts);
+  team_sync<C::TEAM>(team);
+  dit_mid<LOGH, C::NP - 2>(tw, lt, team, lds, sts);
+}
+
 // z = DIT_H( DIF_H(x) . S ), x from IN(j), z delivered to OUT(k, z_k) (unnormalised).
 // The first DIF pass reads IN, the innermost DIF pass + spectrum multiply +
 // innermost DIT pass are one register pass, the last DIT pass hands results to OUT.
-template <int LOGH, class IN, class OUT>
+template <int LOGH, bool OUTLINE = false, class IN, class OUT>
 __device__ __forceinline__ void conv_half(double2* X, const double2* tw, const double2* S, int lt,
                                           int team, IN in, OUT out) {
   using C = Cfg<LOGH>;
@@ -271,10 +301,19 @@ __device__ __forceinline__ void conv_half(double2* X, const double2* tw, const d
     pass<RL, 2, C::H, C::M, nL, C::TEAM>(tw, S, lt, in, out);
     team_sync<C::TEAM>(team);
   } else {
-    dif_chain<LOGH, 0>(tw, lt, team, in, lds, sts);
-    pass<RL, 2, C::H, C::M, nL, C::TEAM>(tw, S, lt, lds, sts);
-    team_sync<C::TEAM>(team);
-    dit_chain<LOGH, C::NP - 2>(tw, lt, team, out, lds, sts);
+    if constexpr (OUTLINE) {
+      constexpr int R0 = 1 << C::lr(0);
+      pass<R0, 0, C::H, C::M, C::H, C::TEAM>(tw, nullptr, lt, in, sts);
+      team_sync<C::TEAM>(team);
+      conv_middle<LOGH>(X, tw, S, lt, team);
+      pass<R0, 1, C::H, C::M, C::H, C::TEAM>(tw, nullptr, lt, lds, out);
+      team_sync<C::TEAM>(team);
+    } else {
+      dif_chain<LOGH, 0>(tw, lt, team, in, lds, sts);
+      pass<RL, 2, C::H, C::M, nL, C::TEAM>(tw, S, lt, lds, sts);
+      team_sync<C::TEAM>(team);
+      dit_chain<LOGH, C::NP - 2>(tw, lt, team, out, lds, sts);
+    }
   }
 }
 
@@ -288,7 +327,7 @@ __device__ __forceinline__ int fbin(int k, int N) { return k >= 0 ? k : k + N; }
 // Bluestein DFT_N of x (fx(n), n < N): forward (conj chirp, spec f) or inverse
 // (chirp, spec i).  Half 1 leaves z1 in scr; half 0 calls fin(k, y_k) with the
 // merged y[k] = z0[k] + w^-k z1[k] (unnormalised; DFT = chirp' . y / M).
-template <int LOGH, bool INV, class FX, class FIN>
+template <int LOGH, bool INV, bool OUTLINE = false, class FX, class FIN>
 __device__ __forceinline__ void bluestein(double2* X, const double2* tw, double2* scr,
                                           const FftArgs& a, int lt, int team, FX fx, FIN fin) {
   using C = Cfg<LOGH>;
@@ -313,8 +352,8 @@ __device__ __forceinline__ void bluestein(double2* X, const double2* tw, double2
   };
   auto out1 = [&](int k, double2 v) { scr[k] = v; };
   auto out0 = [&](int k, double2 v) { fin(k, cadd(v, cmulc(scr[k], omega(tw, k, C::M)))); };
-  conv_half<LOGH>(X, tw, spec + C::H, lt, team, in1, out1);
-  conv_half<LOGH>(X, tw, spec, lt, team, in0, out0);
+  conv_half<LOGH, OUTLINE>(X, tw, spec + C::H, lt, team, in1, out1);
+  conv_half<LOGH, OUTLINE>(X, tw, spec, lt, team, in0, out0);
 }
 
 // Per-CTA setup shared by the stage kernels: team split, buffers, twiddles.
@@ -325,7 +364,7 @@ __device__ __forceinline__ void bluestein(double2* X, const double2* tw, double2
   double2* X = sm + team * C::H;                                             \
   double2* tws = sm + C::NR * C::H;                                          \
   load_tw(tws, a);                                                           \
-  double2* scr = a.scratch + ((long long)blockIdx.x * C::NR + team) * 2 * C::H;
+  double2* scr = a.scratch + ((long long)blockIdx.x * C::NR + team) * 3 * C::H;
 
 // ------------------------------------------------------------------ kernels
 
@@ -378,8 +417,6 @@ __global__ void __launch_bounds__(kT, 1) k_phi_fwd(FftArgs a) {
 // (F_{m,-m'} = eps_m F_{m,m'}, mw.py:400-401), and consecutive orders m, m+1
 // have opposite signs, so the transform of S_1 + i S_2 separates exactly:
 // z = y_1 + i y_2 and eps_1 z[N-1-t] = y_1[t] - i y_2[t].
-// (The forward stage keeps one row per transform: pairing it measured slower,
-// its kernel outgrew the instruction cache.)
 // Tasks pair the orders of magnitude 2k and 2k+1 within the +m block and
 // within the -m block, so a sharded order range [m0, m1) with even bounds
 // pairs exactly as the whole plane does (bit-identical shards).
@@ -407,61 +444,124 @@ __device__ __forceinline__ int theta_task(int q, int m0, int m1, bool real, int&
 // theta stage of the forward transform for each order row (m from row_order):
 // extension (mw.py:161-177), DFT_N + twist (:180-192), weight correlation
 // (:244-251) and m' fold (:273-285, 504-511), written in the forward core's
-// staging layout gfT (ldw columns, +m / -m halves).
+// staging layout gfT (ldw columns, +m / -m halves).  Two rows per Bluestein
+// transform: the extended sequence x of order m satisfies x[N-1-n] = eps_m x[n]
+// except at the self-mirrored n = L-1, so its DFT obeys
+//   Z[-k] e^{2 pi i k/N} = eps_m Z[k] + (1 - eps_m) x[L-1] (-1)^k e^{i pi k/N},
+// and with eps_{m+1} = -eps_m the transform of x_m + i x_{m+1} separates.
 template <bool REAL, int LOGH>
 __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
   FFT_PROLOGUE
-  double2* scrF = scr + C::H;  // F_raw (N <= H)
+  double2* scrF[2] = {scr + C::H, scr + 2 * C::H};  // F of the task's rows (N <= H)
   const int L = a.L, N = a.N, ldw = a.ldw;
   constexpr int H = C::H, M = C::M;
-  for (int row = blockIdx.x * C::NR + team; row < a.nrows * a.nmaps; row += gridDim.x * C::NR) {
-    const int map = row / a.nrows, r = row - map * a.nrows;
-    const int m = row_order(r, a.m0, a.m1, REAL);
-    const bool neg = !REAL && m < 0;
-    const int am = neg ? -m : m;
-    const double eps = (((m + (REAL ? 0 : a.spin)) & 1) ? -1.0 : 1.0);
-    const double2* g = (const double2*)a.in + (long long)map * a.in_stride +
-                       (long long)(REAL ? m : fbin(m, N)) * L;
-    // 1. Bluestein DFT_N of the periodic extension; F_raw[k] = y[k] conj(c[k]) tau(f(k))/M
-    bluestein<LOGH, false>(
+  const int ntask = theta_tasks(a.m0, a.m1, REAL);
+  for (int task = blockIdx.x * C::NR + team; task < ntask * a.nmaps; task += gridDim.x * C::NR) {
+    const int map = task / ntask, q = task - map * ntask;
+    int i1;
+    const bool two = theta_task(q, a.m0, a.m1, REAL, i1) == 2;
+    int mr[2];
+    double eps[2];
+    const double2* g[2];
+    for (int u = 0; u < 2; u++) {
+      mr[u] = row_order(two ? i1 + u : i1, a.m0, a.m1, REAL);
+      eps[u] = (((mr[u] + (REAL ? 0 : a.spin)) & 1) ? -1.0 : 1.0);
+      g[u] = (const double2*)a.in + (long long)map * a.in_stride +
+             (long long)(REAL ? mr[u] : fbin(mr[u], N)) * L;
+    }
+    // 1. Bluestein DFT_N of the periodic extension(s): X[k] = M Z[k]
+    auto ext = [&](int u, int n) { return n < L ? g[u][n] : cscale(g[u][2 * L - 2 - n], eps[u]); };
+    bluestein<LOGH, false, true>(
         X, tws, scr, a, lt, team,
-        [&](int n) { return n < L ? g[n] : cscale(g[2 * L - 2 - n], eps); },
+        [&](int n) {
+          const double2 x1 = ext(0, n);
+          if (!two) return x1;
+          const double2 x2 = ext(1, n);
+          return make_double2(x1.x - x2.y, x1.y + x2.x);  // x1 + i x2
+        },
         [&](int k, double2 y) {
-          if (k < N) scrF[k] = cmul(y, a.rho[k]);
+          if (k < N) X[phys(k)] = cmulc(y, a.chirp[k]);
         });
     team_sync<C::TEAM>(team);
-    // 2. weight correlation on F placed in FFT order (f at f mod M)
-    auto Fpl = [&](int p) -> double2 {
-      if (p < L) return scrF[p];
-      if (p >= M - L + 1) return scrF[p - M + N];
-      return make_double2(0.0, 0.0);
-    };
-    conv_half<LOGH>(
-        X, tws, a.specw + H, lt, team,
-        [&](int j) { return cmul(csub(Fpl(j), Fpl(j + H)), omega(tws, j, M)); },
-        [&](int k, double2 v) { scr[k] = v; });
-    conv_half<LOGH>(
-        X, tws, a.specw, lt, team, [&](int j) { return cadd(Fpl(j), Fpl(j + H)); },
-        [&](int k, double2 v) { X[phys(k)] = v; });
-    team_sync<C::TEAM>(team);
-    // 3. G(m') = y[m' mod M]/M; fold gf[j] = G(j) + s G(-j); write staging column
-    const double sig = eps;  // (-1)^(m+s) (complex) / (-1)^m (real), mw.py:273-285
-    const double inv = 1.0 / (double)M;
-    double2* gT = (double2*)a.out + (long long)map * a.out_stride + (neg ? (long long)L * ldw : 0);
-    for (int j = lt; j < L; j += C::TEAM) {
-      double2 v = cadd(X[phys(j)], cmulc(scr[j], omega(tws, j, M)));
-      if (j > 0) {
-        const int k = H - j;  // position M - j = k + H
-        const double2 u = csub(X[phys(k)], cmulc(scr[k], omega(tws, k, M)));
-        v = make_double2(v.x + sig * u.x, v.y + sig * u.y);
+    // 2. separate the two rows; F[k] = Z[k] tau(f(k)) / (2 pi N)
+    {
+      double2 cc = make_double2(0.0, 0.0);  // M (1 - eps_u) x_u[L-1] (i for the second row)
+      if (two) {
+        const double2 c1 = g[0][L - 1], c2 = g[1][L - 1];
+        cc = eps[0] < 0 ? make_double2(2.0 * M * c1.x, 2.0 * M * c1.y)
+                        : make_double2(-2.0 * M * c2.y, 2.0 * M * c2.x);
       }
-      v = cscale(v, inv);
-      if (neg && (j & 1)) v = make_double2(-v.x, -v.y);
-      gT[blk<kTileCols>(j, am, L)] = v;
-      if (!REAL && m == 0)
-        gT[(long long)L * ldw + blk<kTileCols>(j, 0, L)] = (j & 1) ? make_double2(-v.x, -v.y) : v;
+      // four elements per thread and pass: the table loads (L2) of a pass are in flight together
+      constexpr int U = 4;
+      for (int k0 = lt; k0 < N; k0 += U * C::TEAM) {
+        double2 r2[U], wk[U], ck[U];
+#pragma unroll
+        for (int v = 0; v < U; v++) {
+          const int k = min(k0 + v * C::TEAM, N - 1);
+          r2[v] = __ldg(&a.rho2[k]);
+          if (two) {
+            wk[v] = __ldg(&a.wnk[k]);
+            ck[v] = __ldg(&a.cen[k]);
+          }
+        }
+#pragma unroll
+        for (int v = 0; v < U; v++) {
+          const int k = k0 + v * C::TEAM;
+          if (k >= N) break;
+          const double2 zk = X[phys(k)];
+          if (!two) {
+            scrF[0][k] = cmul(zk, r2[v]);
+            continue;
+          }
+          const double2 zn = X[phys(k ? N - k : 0)];
+          const double2 bk = csub(cmul(zn, wk[v]), cmul(cc, ck[v]));
+          const double2 eb = cscale(bk, eps[0]);
+          const double2 s1 = cadd(zk, eb), s2 = csub(zk, eb);  // 2 Z_1, 2i Z_2
+          scrF[0][k] = cscale(cmul(s1, r2[v]), 0.5);
+          scrF[1][k] = cscale(cmul(make_double2(s2.y, -s2.x), r2[v]), 0.5);
+        }
+      }
     }
     team_sync<C::TEAM>(team);
+    for (int u = 0; u < (two ? 2 : 1); u++) {
+      const double2* F = scrF[u];
+      const int m = mr[u];
+      const bool neg = !REAL && m < 0;
+      const int am = neg ? -m : m;
+      // 3. weight correlation on F placed in FFT order (f at f mod M)
+      auto Fpl = [&](int p) -> double2 {
+        if (p < L) return F[p];
+        if (p >= M - L + 1) return F[p - M + N];
+        return make_double2(0.0, 0.0);
+      };
+      conv_half<LOGH, true>(
+          X, tws, a.specw + H, lt, team,
+          [&](int j) { return cmul(csub(Fpl(j), Fpl(j + H)), omega(tws, j, M)); },
+          [&](int k, double2 v) { scr[k] = v; });
+      conv_half<LOGH, true>(
+          X, tws, a.specw, lt, team, [&](int j) { return cadd(Fpl(j), Fpl(j + H)); },
+          [&](int k, double2 v) { X[phys(k)] = v; });
+      team_sync<C::TEAM>(team);
+      // 4. G(m') = y[m' mod M]/M; fold gf[j] = G(j) + s G(-j); write staging column
+      const double sig = eps[u];  // (-1)^(m+s) (complex) / (-1)^m (real), mw.py:273-285
+      const double inv = 1.0 / (double)M;
+      double2* gT =
+          (double2*)a.out + (long long)map * a.out_stride + (neg ? (long long)L * ldw : 0);
+      for (int j = lt; j < L; j += C::TEAM) {
+        double2 v = cadd(X[phys(j)], cmulc(scr[j], omega(tws, j, M)));
+        if (j > 0) {
+          const int k = H - j;  // position M - j = k + H
+          const double2 w = csub(X[phys(k)], cmulc(scr[k], omega(tws, k, M)));
+          v = make_double2(v.x + sig * w.x, v.y + sig * w.y);
+        }
+        v = cscale(v, inv);
+        if (neg && (j & 1)) v = make_double2(-v.x, -v.y);
+        gT[blk<kTileCols>(j, am, L)] = v;
+        if (!REAL && m == 0)
+          gT[(long long)L * ldw + blk<kTileCols>(j, 0, L)] = (j & 1) ? make_double2(-v.x, -v.y) : v;
+      }
+      team_sync<C::TEAM>(team);
+    }
   }
 }
 

@@ -85,7 +85,7 @@ struct mwsht_plan {
   // fused FFT engine (fft.cu): M-point FFT-convolutions in H = M/2 smem halves
   int M = 0, H = 0, logH = 0, nsm = 0;
   double2 *tw = nullptr, *chirp = nullptr, *specf = nullptr, *speci = nullptr, *specw = nullptr,
-          *rho = nullptr, *scratch = nullptr;
+          *rho = nullptr, *scratch = nullptr, *cen = nullptr, *wnk = nullptr, *rho2 = nullptr;
   double2 *bufA = nullptr, *bufB = nullptr, *bufG = nullptr;
   long long strideA = 0, strideB = 0, strideG = 0;
   unsigned long long* red = nullptr;       // 2 device slots for the reality check (kept zero)
@@ -386,7 +386,9 @@ static int range_tiles(mwsht_plan* p, int m0, int m1, mwsht_plan::TileSet** out)
 // spectra (half-split DIF of the Bluestein kernels c, conj c and of the
 // weight-correlation kernel K'[d mod M] = 2 pi w(-d), |d| <= 2L-2,
 // quadrature.py:66-74, mw.py:237-238), and the forward theta glue
-// rho[k] = conj(c[k]) e^{-i f(k) pi/N} / (2 pi N M), f(k) = k (k < L), k - N.
+// rho[k] = conj(c[k]) e^{-i f(k) pi/N} / (2 pi N M), f(k) = k (k < L), k - N,
+// and for the paired forward theta rows (fft.cu): cen[k] = (-1)^k e^{i pi k/N},
+// wnk[k] = e^{2 pi i k/N}, rho2[k] = e^{-i f(k) pi/N} / (2 pi N M).
 static fft::FftArgs fft_args(mwsht_plan* p) {
   fft::FftArgs a{};
   a.L = p->L;
@@ -401,6 +403,9 @@ static fft::FftArgs fft_args(mwsht_plan* p) {
   a.speci = p->speci;
   a.specw = p->specw;
   a.rho = p->rho;
+  a.cen = p->cen;
+  a.wnk = p->wnk;
+  a.rho2 = p->rho2;
   a.scratch = p->scratch;
   a.nmaps = 1;
   a.m0 = 0;
@@ -421,6 +426,7 @@ static int build_fft_tables(mwsht_plan* p) {
   if (p->H > 8192) return fail(MWSHT_E_BAND_LIMIT, "plan_create", "fused FFT engine supports L <= 4096");
   const ld PI = 3.141592653589793238462643383279502884L;
   std::vector<double2> tw(M / 4 + 1), ch(N), rho(N), kf(M, make_double2(0, 0)), ki(kf), kw(kf);
+  std::vector<double2> cen(N), wnk(N), rho2(N);
   for (int j = 0; j <= M / 4; j++) {
     const ld a = -2.0L * PI * (ld)j / (ld)M;
     tw[j] = make_double2((double)cosl(a), (double)sinl(a));
@@ -442,6 +448,10 @@ static int build_fft_tables(mwsht_plan* p) {
     const ld tr = cosl(a) * sc, ti = sinl(a) * sc;
     // conj(c) * tau
     rho[k] = make_double2((double)(cr[k] * tr + ci[k] * ti), (double)(cr[k] * ti - ci[k] * tr));
+    rho2[k] = make_double2((double)tr, (double)ti);
+    const ld b = PI * (ld)k / (ld)N, sg = (k & 1) ? -1.0L : 1.0L;
+    cen[k] = make_double2((double)(sg * cosl(b)), (double)(sg * sinl(b)));
+    wnk[k] = make_double2((double)cosl(2.0L * b), (double)sinl(2.0L * b));
   }
   for (int j = -(N - 1); j <= N - 1; j++) {
     const int n = j < 0 ? -j : j;
@@ -462,7 +472,8 @@ static int build_fft_tables(mwsht_plan* p) {
   }
   int rc;
   if ((rc = upload(p, &p->tw, tw)) || (rc = upload(p, &p->chirp, ch)) ||
-      (rc = upload(p, &p->rho, rho)))
+      (rc = upload(p, &p->rho, rho)) || (rc = upload(p, &p->cen, cen)) ||
+      (rc = upload(p, &p->wnk, wnk)) || (rc = upload(p, &p->rho2, rho2)))
     return rc;
   double2 *dkf, *dki, *dkw;
   if ((rc = upload(p, &dkf, kf)) || (rc = upload(p, &dki, ki)) || (rc = upload(p, &dkw, kw)))
@@ -480,8 +491,8 @@ static int build_fft_tables(mwsht_plan* p) {
   int dev;
   CU(cudaGetDevice(&dev));
   CU(cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, dev));
-  // per CTA: NR teams x 2H complex, NR*H <= 8192 for every size (fft.cu Cfg)
-  if ((rc = dev_alloc(p, (void**)&p->scratch, sizeof(double2) * 16384 * (size_t)p->nsm)))
+  // per CTA: NR teams x 3H complex, NR*H <= 8192 for every size (fft.cu Cfg)
+  if ((rc = dev_alloc(p, (void**)&p->scratch, sizeof(double2) * 3 * 8192 * (size_t)p->nsm)))
     return rc;
   return MWSHT_OK;
 }
