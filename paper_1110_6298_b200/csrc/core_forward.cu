@@ -360,8 +360,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
 template <bool REAL, bool SPIN0>
 static void launch_fwd(const FwdArgs& a, dim3 grid, cudaStream_t st) {
   const size_t smem = sizeof(fwd::Smem);
-  cudaFuncSetAttribute(k_forward_core<REAL, SPIN0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
+  smem_attr_once((const void*)k_forward_core<REAL, SPIN0>, smem);
   k_forward_core<REAL, SPIN0><<<grid, kCoreThreadsWS, smem, st>>>(a);
 }
 

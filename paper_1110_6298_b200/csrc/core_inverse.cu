@@ -378,8 +378,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
 template <bool REAL, bool SPIN0>
 static void launch_inv(const InvArgs& a, dim3 grid, cudaStream_t st) {
   const size_t smem = sizeof(inv::Smem);
-  cudaFuncSetAttribute(k_inverse_core<REAL, SPIN0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
+  smem_attr_once((const void*)k_inverse_core<REAL, SPIN0>, smem);
   k_inverse_core<REAL, SPIN0><<<grid, kCoreThreadsWS, smem, st>>>(a);
 }
 

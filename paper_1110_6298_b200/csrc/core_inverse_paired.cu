@@ -452,8 +452,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
 template <bool REAL, bool SPIN0, bool PAIRED>
 static void launch_inv_paired(const InvArgs& a, dim3 grid, cudaStream_t st) {
   const size_t smem = sizeof(invp::Smem<PAIRED ? 8 : kChunk, PAIRED>);
-  cudaFuncSetAttribute(k_inverse_core_paired<REAL, SPIN0, PAIRED>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  smem_attr_once((const void*)k_inverse_core_paired<REAL, SPIN0, PAIRED>, smem);
   k_inverse_core_paired<REAL, SPIN0, PAIRED><<<grid, kCoreThreadsWS, smem, st>>>(a);
 }
 

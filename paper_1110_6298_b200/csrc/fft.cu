@@ -707,7 +707,7 @@ template <int LOGH, class K>
 static void launch_t(K kern, const FftArgs& a, int nsm, cudaStream_t st) {
   using C = Cfg<LOGH>;
   const size_t sm = smem_bytes_t<LOGH>();
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  smem_attr_once((const void*)kern, sm);
   long long rows = (long long)a.nrows * a.nmaps;
   long long grid = (rows + C::NR - 1) / C::NR;
   if (grid > nsm) grid = nsm;
@@ -740,7 +740,7 @@ static void launch_stage(int which, bool real, const FftArgs& a, int nsm, cudaSt
 template <int LOGH>
 static void spectrum_t(const FftArgs& a, const double2* kern, double2* spec, cudaStream_t st) {
   const size_t sm = smem_bytes_t<LOGH>();
-  cudaFuncSetAttribute(k_spectrum<LOGH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  smem_attr_once((const void*)k_spectrum<LOGH>, sm);
   k_spectrum<LOGH><<<1, kT, sm, st>>>(a, kern, spec);
 }
 
