@@ -141,6 +141,7 @@ struct FwdArgs {
   const int2* tiles;
   int out_mode, spin;
   int ldw;
+  int nmaps;  // maps in the batch (set by launch_forward_core)
   long long in_stride, out_stride;
 };
 

@@ -24,14 +24,19 @@
 namespace mwsht {
 
 namespace fwd {
-constexpr int R = kTileRows, C = kTileCols, CH = kChunk, NB = kStages;
+constexpr int R = kTileRows, C = kTileCols, CH = kChunk;
+// MB maps of a batch share every chain (one recursion, MB contractions);
+// their staging rows double the stage size, so the ring is one stage shorter.
+template <int MB>
 struct Stage {
-  double2 q[CH][R];    // (coefficient producing y_{m'-1}, W'(l, m'))
-  double2 gp[CH][C];   // gfold[+m][m']
-  double2 gn[CH][C];   // (-1)^m' gfold[-m][m']
+  double2 q[CH][R];        // (coefficient producing y_{m'-1}, W'(l, m'))
+  double2 gp[MB][CH][C];   // gfold[+m][m']
+  double2 gn[MB][CH][C];   // (-1)^m' gfold[-m][m']
 };
+template <int MB>
 struct Smem {
-  Stage st[NB];
+  static constexpr int NB = MB == 1 ? kStages : kStages - 1;
+  Stage<MB> st[NB];
   double seedy[8][kConsumerThreads];
   uint64_t full[NB], empty[NB];
 };
@@ -53,12 +58,17 @@ __device__ __forceinline__ void rescale(double (&y)[NE], double (&y1)[NE], unsig
 
 // Warp-specialised 384-thread CTA (common.cuh): warpgroup 0 = TMA producer,
 // warpgroups 1-2 = 8 consumer warps with a raised register budget.
-template <bool REAL, bool SPIN0>
+template <bool REAL, bool SPIN0, int MB>
 __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
   constexpr int NI = 4, NJ = 2, NE = NI * NJ;
   constexpr int NG = REAL ? 1 : 2;
+  using Sm = fwd::Smem<MB>;
+  constexpr int NB = Sm::NB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  fwd::Smem& sm = *reinterpret_cast<fwd::Smem*>(smem_raw);
+  Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
+  // maps of this CTA: MB * blockIdx.y + mb (the last pair of an odd batch repeats
+  // its map; that copy's results are not written)
+  auto map_of = [&](int mb) { return min(MB * (int)blockIdx.y + mb, a.nmaps - 1); };
 
   const DevTables& T = a.t;
   const int L = T.L, Lp = a.ldw;
@@ -69,7 +79,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
   const int lane = threadIdx.x & 31, wall = threadIdx.x >> 5;
 
   if (threadIdx.x == 0) {
-    for (int b = 0; b < fwd::NB; b++) {
+    for (int b = 0; b < NB; b++) {
       mbar_init(&sm.full[b], 1);
       mbar_init(&sm.empty[b], kConsumerWarps);
     }
@@ -82,24 +92,30 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
     setmaxnreg_dec<kProducerRegs>();
     if (wall != 0) return;
     // ------------------------------------------------------------ producer
-    const double2* gp = a.gf + (long long)blockIdx.y * a.in_stride;
-    const double2* gn = gp + (long long)L * Lp;
+    const double2* gpm[MB];
+#pragma unroll
+    for (int mb = 0; mb < MB; mb++) gpm[mb] = a.gf + (long long)map_of(mb) * a.in_stride;
     // blocked layouts (common.cuh): the chunk's steps mu = mc .. mc-ns+1 are one
     // contiguous block (ascending mu), placed in stage rows CH-ns .. CH-1 so
     // that step s (mu = mc - s) always sits in row CH-1-s
     if (lane == 0) {
       for (int k = 0; k < nchunks; k++) {
-        const int b = k % fwd::NB, mc = mu_top - k * kChunk, ns = min(kChunk, mc + 1);
-        if (k >= fwd::NB) mbar_wait(&sm.empty[b], ((k / fwd::NB) - 1) & 1);
+        const int b = k % NB, mc = mu_top - k * kChunk, ns = min(kChunk, mc + 1);
+        if (k >= NB) mbar_wait(&sm.empty[b], ((k / NB) - 1) & 1);
         fence_proxy_async();
-        mbar_arrive_expect_tx(&sm.full[b], ns * (fwd::R * 16u + NG * fwd::C * 16u));
-        fwd::Stage& S = sm.st[b];
+        mbar_arrive_expect_tx(&sm.full[b], ns * (fwd::R * 16u + MB * NG * fwd::C * 16u));
+        auto& S = sm.st[b];
         const int mlo = mc - ns + 1;
         const long long oc = blk<fwd::C>(mlo, c0, L);
         bulk_g2s(&S.q[fwd::CH - ns][0], a.rowtab + blk<fwd::R>(mlo, l0b, L), ns * fwd::R * 16,
                  &sm.full[b]);
-        bulk_g2s(&S.gp[fwd::CH - ns][0], gp + oc, ns * fwd::C * 16, &sm.full[b]);
-        if (!REAL) bulk_g2s(&S.gn[fwd::CH - ns][0], gn + oc, ns * fwd::C * 16, &sm.full[b]);
+#pragma unroll
+        for (int mb = 0; mb < MB; mb++) {
+          bulk_g2s(&S.gp[mb][fwd::CH - ns][0], gpm[mb] + oc, ns * fwd::C * 16, &sm.full[b]);
+          if (!REAL)
+            bulk_g2s(&S.gn[mb][fwd::CH - ns][0], gpm[mb] + (long long)L * Lp + oc,
+                     ns * fwd::C * 16, &sm.full[b]);
+        }
       }
     }
     return;
@@ -108,7 +124,6 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
   // -------------------------------------------------------------- consumers
   setmaxnreg_inc<kConsumerRegs>();
   const int w = wall - 4, tid = threadIdx.x - 128;
-  double2* __restrict__ out = a.out + (long long)blockIdx.y * a.out_stride;
   const int wr = w & 3, wc = w >> 2, r = lane & 3, c = lane >> 2, par = wr & 1;
   int rl[NI], cl[NJ], ll[NI], mm[NJ];
   double md[NJ];
@@ -146,13 +161,15 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
       slv |= (unsigned)lev << (4 * e);
     }
 
-  double y[NE], y1[NE], acc[NE][2 * NG];
+  double y[NE], y1[NE], acc[MB][NE][2 * NG];
 #pragma unroll
   for (int e = 0; e < NE; e++) {
     y[e] = 0.0;
     y1[e] = 0.0;
 #pragma unroll
-    for (int k = 0; k < 2 * NG; k++) acc[e][k] = 0.0;
+    for (int mb = 0; mb < MB; mb++)
+#pragma unroll
+      for (int k = 0; k < 2 * NG; k++) acc[mb][e][k] = 0.0;
   }
   unsigned lv = 0;
 
@@ -164,13 +181,14 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
   bool fast = false, started = false;
 
   for (int k = 0; k < nchunks; k++) {
-    const int b = k % fwd::NB, mc = mu_top - k * kChunk, ns = min(kChunk, mc + 1);
-    mbar_wait(&sm.full[b], (k / fwd::NB) & 1);
+    const int b = k % NB, mc = mu_top - k * kChunk, ns = min(kChunk, mc + 1);
+    mbar_wait(&sm.full[b], (k / NB) & 1);
     // rl[i] = rl0 + 8 i, cl[j] = cl0 + 8 j: one base pointer per array and chunk
-    const fwd::Stage& S = sm.st[b];
+    const auto& S = sm.st[b];
     const double2* rowp = &S.q[fwd::CH - 1][0] + rl0;  // step s at row CH-1-s
-    const double2* gpp = &S.gp[fwd::CH - 1][0] + cl0;
-    const double2* gnp = &S.gn[fwd::CH - 1][0] + cl0;
+    const double2* gpp = &S.gp[0][fwd::CH - 1][0] + cl0;
+    const double2* gnp = &S.gn[0][fwd::CH - 1][0] + cl0;
+    constexpr int MS = fwd::CH * fwd::C;  // distance between maps' staging rows
 
     if (warp_has && wrow_hi >= mc - ns + 1) {
       if (!started) {
@@ -225,14 +243,16 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
             }
         };
         auto full_step = [&](auto masked, int s) {
-          double2 qp[NI], g[NJ][NG];
+          double2 qp[NI], g[MB][NJ][NG];
 #pragma unroll
           for (int i = 0; i < NI; i++) qp[i] = rowp[-s * fwd::R + 8 * i];
 #pragma unroll
-          for (int j = 0; j < NJ; j++) {
-            g[j][0] = gpp[-s * fwd::C + 8 * j];
-            if (!REAL) g[j][NG - 1] = gnp[-s * fwd::C + 8 * j];
-          }
+          for (int mb = 0; mb < MB; mb++)
+#pragma unroll
+            for (int j = 0; j < NJ; j++) {
+              g[mb][j][0] = gpp[mb * MS - s * fwd::C + 8 * j];
+              if (!REAL) g[mb][j][NG - 1] = gnp[mb * MS - s * fwd::C + 8 * j];
+            }
 #pragma unroll
           for (int i = 0; i < NI; i++)
 #pragma unroll
@@ -241,10 +261,12 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
               double t = y[e] * qp[i].y;
               if (decltype(masked)::value) t = ((live >> e) & 1u) ? t : 0.0;
 #pragma unroll
-              for (int k2 = 0; k2 < NG; k2++) {
-                acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
-                acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
-              }
+              for (int mb = 0; mb < MB; mb++)
+#pragma unroll
+                for (int k2 = 0; k2 < NG; k2++) {
+                  acc[mb][e][2 * k2] = fma(t, g[mb][j][k2].x, acc[mb][e][2 * k2]);
+                  acc[mb][e][2 * k2 + 1] = fma(t, g[mb][j][k2].y, acc[mb][e][2 * k2 + 1]);
+                }
               const double yn = fma(md[j] * qp[i].x, y[e], -y1[e]);
               y1[e] = y[e];
               y[e] = yn;
@@ -312,6 +334,10 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
   // ---------------------------------------------------------------- epilogue
   const double sgs = (a.spin & 1) ? -1.0 : 1.0;
 #pragma unroll
+  for (int mb = 0; mb < MB; mb++) {
+  if (MB * (int)blockIdx.y + mb >= a.nmaps) break;
+  double2* __restrict__ out = a.out + (long long)map_of(mb) * a.out_stride;
+#pragma unroll
   for (int i = 0; i < NI; i++) {
     const int l = ll[i];
     if (l >= L) continue;
@@ -321,7 +347,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
       const int m = mm[j];
       if (m > l) continue;
       const int e = i * NJ + j;
-      const double2 Rp = make_double2(acc[e][0], acc[e][1]);
+      const double2 Rp = make_double2(acc[mb][e][0], acc[mb][e][1]);
       if (a.out_mode == 1) {
         if (REAL) {
           out[(long long)l * L + m] = Rp;
@@ -330,7 +356,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
           out[(long long)l * N + (L - 1 + m)] = Rp;
           if (m > 0) {
             const double sl = (l & 1) ? -1.0 : 1.0;
-            out[(long long)l * N + (L - 1 - m)] = make_double2(sl * acc[e][2], sl * acc[e][3]);
+            out[(long long)l * N + (L - 1 - m)] = make_double2(sl * acc[mb][e][2], sl * acc[mb][e][3]);
           }
         }
         continue;
@@ -349,29 +375,42 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
         out[base + m] = cscale(cmul(Rp, ipow(m + a.spin)), sgs * clv);
         if (m > 0) {
           const double sl = (l & 1) ? -1.0 : 1.0;
-          const double2 Rn = make_double2(sl * acc[e][2], sl * acc[e][3]);
+          const double2 Rn = make_double2(sl * acc[mb][e][2], sl * acc[mb][e][3]);
           out[base - m] = cscale(cmul(Rn, ipow(a.spin - m)), sgs * clv);
         }
       }
     }
   }
 }
-
-template <bool REAL, bool SPIN0>
-static void launch_fwd(const FwdArgs& a, dim3 grid, cudaStream_t st) {
-  const size_t smem = sizeof(fwd::Smem);
-  smem_attr_once((const void*)k_forward_core<REAL, SPIN0>, smem);
-  k_forward_core<REAL, SPIN0><<<grid, kCoreThreadsWS, smem, st>>>(a);
 }
 
-void launch_forward_core(const FwdArgs& a, int ntiles, int nmaps, bool real, cudaStream_t st) {
-  dim3 grid(ntiles, nmaps);
+template <bool REAL, bool SPIN0, int MB>
+static void launch_fwd(const FwdArgs& a, int ntiles, cudaStream_t st) {
+  const size_t smem = sizeof(fwd::Smem<MB>);
+  smem_attr_once((const void*)k_forward_core<REAL, SPIN0, MB>, smem);
+  dim3 grid(ntiles, (a.nmaps + MB - 1) / MB);
+  k_forward_core<REAL, SPIN0, MB><<<grid, kCoreThreadsWS, smem, st>>>(a);
+}
+
+template <int MB>
+static void launch_fwd_mb(const FwdArgs& a, int ntiles, bool real, cudaStream_t st) {
   if (real)
-    launch_fwd<true, true>(a, grid, st);
+    launch_fwd<true, true, MB>(a, ntiles, st);
   else if (a.spin == 0)
-    launch_fwd<false, true>(a, grid, st);
+    launch_fwd<false, true, MB>(a, ntiles, st);
   else
-    launch_fwd<false, false>(a, grid, st);
+    launch_fwd<false, false, MB>(a, ntiles, st);
+}
+
+// Batches of two or more maps run two maps per CTA: each chain's recursion
+// then feeds both maps' contractions.
+void launch_forward_core(const FwdArgs& a0, int ntiles, int nmaps, bool real, cudaStream_t st) {
+  FwdArgs a = a0;
+  a.nmaps = nmaps;
+  if (nmaps >= 2)
+    launch_fwd_mb<2>(a, ntiles, real, st);
+  else
+    launch_fwd_mb<1>(a, ntiles, real, st);
 }
 
 }  // namespace mwsht
