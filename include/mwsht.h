@@ -175,7 +175,8 @@ int mwsht_shard_inverse_phi(mwsht_plan *plan, const void *OUT, int t0, int t1, v
  * Paired tiles: each (m', m) chain with m' > m also produces the transposed
  * output T[m, m'] (Delta^l_{m m'} = (-1)^(m'-m) Delta^l_{m' m}), so one
  * recursion feeds two contractions.  Spin 0 only.  mode 0: plain tiles
- * everywhere; mode 1 or -1 (default): paired tiles for spin 0.  Results
+ * everywhere; mode -1 (default): paired tiles for single spin-0 maps (batches share the
+ * recursion between maps instead); mode 1: paired for every spin-0 call.  Results
  * agree to rounding (tests/test_gpu_paired.py). */
 int mwsht_plan_set_paired(mwsht_plan *plan, int mode);
 

@@ -130,6 +130,7 @@ struct InvArgs {
   int out_mode, spin;
   int ldw;
   int paired;                      // tiles cover the lower triangle and also emit the transpose
+  int nmaps;                       // maps in the batch (set by launch_inverse_core)
   long long g_stride, out_stride;  // per-map element strides (batch = gridDim.y)
 };
 

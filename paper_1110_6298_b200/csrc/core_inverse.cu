@@ -28,15 +28,20 @@ namespace mwsht {
 
 
 namespace inv {
-constexpr int R = kTileRows, C = kTileCols, CH = kChunk, NB = kStages;
+constexpr int R = kTileRows, C = kTileCols, CH = kChunk;
+// MB maps of a batch share every chain (one recursion, MB contractions);
+// their staging rows enlarge the stage, so the ring is one stage shorter.
+template <int MB>
 struct Stage {
-  double2 row[CH][R];  // (kap_l C_l(m'), W_l(m'))
-  double colc[CH][C];  // C_l(m)
-  double2 gp[CH][C];   // c_l u_l(m) f_{l,m}
-  double2 gn[CH][C];   // c_l u_l(m) (-1)^l f_{l,-m}
+  double2 row[CH][R];      // (kap_l C_l(m'), W_l(m'))
+  double colc[CH][C];      // C_l(m)
+  double2 gp[MB][CH][C];   // c_l u_l(m) f_{l,m}
+  double2 gn[MB][CH][C];   // c_l u_l(m) (-1)^l f_{l,-m}
 };
+template <int MB>
 struct Smem {
-  Stage st[NB];
+  static constexpr int NB = MB == 1 ? kStages : kStages - 1;
+  Stage<MB> st[NB];
   double seedz[8][kConsumerThreads];
   uint64_t full[NB], empty[NB];
 };
@@ -56,12 +61,17 @@ __device__ __forceinline__ void rescale(double (&z)[NE], double (&zp)[NE], unsig
   }
 }
 
-template <bool REAL, bool SPIN0>
+template <bool REAL, bool SPIN0, int MB>
 __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
   constexpr int NI = 4, NJ = 2, NE = NI * NJ;
   constexpr int NG = REAL ? 1 : 2;  // complex g values per column: f_{l,m} (+ f_{l,-m})
+  using Sm = inv::Smem<MB>;
+  constexpr int NB = Sm::NB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  inv::Smem& sm = *reinterpret_cast<inv::Smem*>(smem_raw);
+  Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
+  // maps of this CTA: MB * blockIdx.y + mb (the last pair of an odd batch repeats
+  // its map; that copy's results are not written)
+  auto map_of = [&](int mb) { return min(MB * (int)blockIdx.y + mb, a.nmaps - 1); };
 
   const DevTables& T = a.t;
   const int L = T.L, N = T.N, Lp = a.ldw;
@@ -72,7 +82,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
   const int lane = threadIdx.x & 31, wall = threadIdx.x >> 5;
 
   if (threadIdx.x == 0) {
-    for (int b = 0; b < inv::NB; b++) {
+    for (int b = 0; b < NB; b++) {
       mbar_init(&sm.full[b], 1);
       mbar_init(&sm.empty[b], kConsumerWarps);
     }
@@ -86,21 +96,28 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
     if (wall != 0) return;
     // ------------------------------------------------------------ producer
     const double2* rowtab = a.rowtab;
-    const double2* gp = a.gp + (long long)blockIdx.y * a.g_stride;
-    const double2* gn = gp + (long long)L * Lp;
+    const double2* gpm[MB];
+#pragma unroll
+    for (int mb = 0; mb < MB; mb++) gpm[mb] = a.gp + (long long)map_of(mb) * a.g_stride;
     // blocked layouts (common.cuh): a chunk is one contiguous copy per array
     if (lane == 0) {
       for (int k = 0; k < nchunks; k++) {
-        const int b = k % inv::NB, lc = lstart + k * kChunk, ns = min(kChunk, L - lc);
-        if (k >= inv::NB) mbar_wait(&sm.empty[b], ((k / inv::NB) - 1) & 1);
+        const int b = k % NB, lc = lstart + k * kChunk, ns = min(kChunk, L - lc);
+        if (k >= NB) mbar_wait(&sm.empty[b], ((k / NB) - 1) & 1);
         fence_proxy_async();
-        mbar_arrive_expect_tx(&sm.full[b], ns * (inv::R * 16u + inv::C * 8u + NG * inv::C * 16u));
-        inv::Stage& S = sm.st[b];
+        mbar_arrive_expect_tx(&sm.full[b],
+                              ns * (inv::R * 16u + inv::C * 8u + MB * NG * inv::C * 16u));
+        auto& S = sm.st[b];
         const long long oc = blk<inv::C>(lc, c0, L);
         bulk_g2s(&S.row[0][0], rowtab + blk<inv::R>(lc, r0, L), ns * inv::R * 16, &sm.full[b]);
         bulk_g2s(&S.colc[0][0], a.colc + oc, ns * inv::C * 8, &sm.full[b]);
-        bulk_g2s(&S.gp[0][0], gp + oc, ns * inv::C * 16, &sm.full[b]);
-        if (!REAL) bulk_g2s(&S.gn[0][0], gn + oc, ns * inv::C * 16, &sm.full[b]);
+#pragma unroll
+        for (int mb = 0; mb < MB; mb++) {
+          bulk_g2s(&S.gp[mb][0][0], gpm[mb] + oc, ns * inv::C * 16, &sm.full[b]);
+          if (!REAL)
+            bulk_g2s(&S.gn[mb][0][0], gpm[mb] + (long long)L * Lp + oc, ns * inv::C * 16,
+                     &sm.full[b]);
+        }
       }
     }
     return;
@@ -109,7 +126,6 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
   // -------------------------------------------------------------- consumers
   setmaxnreg_inc<kConsumerRegs>();
   const int w = wall - 4, tid = threadIdx.x - 128;
-  double2* __restrict__ out = a.out + (long long)blockIdx.y * a.out_stride;
   const int wr = w & 3, wc = w >> 2, r = lane & 3, c = lane >> 2, par = wr & 1;
   int rl[NI], cl[NJ], mp[NI], mm[NJ];
 #pragma unroll
@@ -149,13 +165,15 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
       slv |= (unsigned)lev << (4 * e);
     }
 
-  double z[NE], zp[NE], acc[NE][2 * NG];
+  double z[NE], zp[NE], acc[MB][NE][2 * NG];
 #pragma unroll
   for (int e = 0; e < NE; e++) {
     z[e] = 0.0;
     zp[e] = 0.0;
 #pragma unroll
-    for (int k = 0; k < 2 * NG; k++) acc[e][k] = 0.0;
+    for (int mb = 0; mb < MB; mb++)
+#pragma unroll
+      for (int k = 0; k < 2 * NG; k++) acc[mb][e][k] = 0.0;
   }
   unsigned lv = 0;  // current levels, 4 bits per chain (0 = true scale)
 
@@ -166,15 +184,16 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
   bool fast = false, started = false;
 
   for (int k = 0; k < nchunks; k++) {
-    const int b = k % inv::NB, lc = lstart + k * kChunk, ns = min(kChunk, L - lc);
-    mbar_wait(&sm.full[b], (k / inv::NB) & 1);
+    const int b = k % NB, lc = lstart + k * kChunk, ns = min(kChunk, L - lc);
+    mbar_wait(&sm.full[b], (k / NB) & 1);
     // rl[i] = rl0 + 8 i, cl[j] = cl0 + 8 j: one base pointer per array and chunk,
     // constant offsets per entry (rl0/cl0 opaque: never rematerialised from %tid)
-    const inv::Stage& S = sm.st[b];
+    const auto& S = sm.st[b];
     const double2* rowp = &S.row[0][0] + rl0;
     const double* colp = &S.colc[0][0] + cl0;
-    const double2* gpp = &S.gp[0][0] + cl0;
-    const double2* gnp = &S.gn[0][0] + cl0;
+    const double2* gpp = &S.gp[0][0][0] + cl0;
+    const double2* gnp = &S.gn[0][0][0] + cl0;
+    constexpr int MS = inv::CH * inv::C;  // distance between maps' staging rows
 
     if (warp_has && wl0_min < lc + ns) {
       if (!started) {
@@ -237,14 +256,17 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
         auto full_step = [&](auto masked, int s) {
           double2 rp[NI];
           double cc[NJ];
-          double2 g[NJ][NG];
+          double2 g[MB][NJ][NG];
 #pragma unroll
           for (int i = 0; i < NI; i++) rp[i] = rowp[s * inv::R + 8 * i];
 #pragma unroll
           for (int j = 0; j < NJ; j++) {
             cc[j] = colp[s * inv::C + 8 * j];
-            g[j][0] = gpp[s * inv::C + 8 * j];
-            if (!REAL) g[j][NG - 1] = gnp[s * inv::C + 8 * j];
+#pragma unroll
+            for (int mb = 0; mb < MB; mb++) {
+              g[mb][j][0] = gpp[mb * MS + s * inv::C + 8 * j];
+              if (!REAL) g[mb][j][NG - 1] = gnp[mb * MS + s * inv::C + 8 * j];
+            }
           }
 #pragma unroll
           for (int i = 0; i < NI; i++)
@@ -254,10 +276,12 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
               double t = z[e] * rp[i].y;
               if (decltype(masked)::value) t = ((live >> e) & 1u) ? t : 0.0;
 #pragma unroll
-              for (int k2 = 0; k2 < NG; k2++) {
-                acc[e][2 * k2] = fma(t, g[j][k2].x, acc[e][2 * k2]);
-                acc[e][2 * k2 + 1] = fma(t, g[j][k2].y, acc[e][2 * k2 + 1]);
-              }
+              for (int mb = 0; mb < MB; mb++)
+#pragma unroll
+                for (int k2 = 0; k2 < NG; k2++) {
+                  acc[mb][e][2 * k2] = fma(t, g[mb][j][k2].x, acc[mb][e][2 * k2]);
+                  acc[mb][e][2 * k2 + 1] = fma(t, g[mb][j][k2].y, acc[mb][e][2 * k2 + 1]);
+                }
               const double zn = fma(rp[i].x * cc[j], z[e], -zp[e]);
               zp[e] = z[e];
               z[e] = zn;
@@ -324,6 +348,10 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
   // ---------------------------------------------------------------- epilogue
   const int sgs = (a.spin & 1) ? -1 : 1;  // (-1)^s
 #pragma unroll
+  for (int mb = 0; mb < MB; mb++) {
+  if (MB * (int)blockIdx.y + mb >= a.nmaps) break;
+  double2* __restrict__ out = a.out + (long long)map_of(mb) * a.out_stride;
+#pragma unroll
   for (int i = 0; i < NI; i++) {
     const int x = mp[i];
     if (x >= L) continue;
@@ -337,7 +365,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
       const int m = mm[j];
       if (m >= L) continue;
       const int e = i * NJ + j;
-      const double2 Tp = make_double2(acc[e][0], acc[e][1]);
+      const double2 Tp = make_double2(acc[mb][e][0], acc[mb][e][1]);
       if (a.out_mode == 1) {
         if (REAL) {
           out[(long long)x * L + m] = Tp;
@@ -345,7 +373,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
           out[(long long)x * N + (L - 1 + m)] = Tp;
           if (m > 0) {
             const double sx = (x & 1) ? -1.0 : 1.0;
-            out[(long long)x * N + (L - 1 - m)] = make_double2(sx * acc[e][2], sx * acc[e][3]);
+            out[(long long)x * N + (L - 1 - m)] = make_double2(sx * acc[mb][e][2], sx * acc[mb][e][3]);
           }
         }
         continue;
@@ -364,7 +392,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
         if (x) rowp[binn] = cscale(cmul(Fp, twc), ((m + a.spin) & 1) ? -1.0 : 1.0);
         if (m > 0) {
           const double sx = (x & 1) ? -1.0 : 1.0;
-          const double2 Tn = make_double2(sx * acc[e][2], sx * acc[e][3]);
+          const double2 Tn = make_double2(sx * acc[mb][e][2], sx * acc[mb][e][3]);
           const double2 Fn = cscale(cmul(Tn, ipow(m - a.spin)), (double)sgs);
           double2* rown = out + (long long)(L - 1 - m) * N;
           rown[binp] = cmul(Fn, tw);
@@ -374,29 +402,42 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
     }
   }
 }
+}
 
-template <bool REAL, bool SPIN0>
-static void launch_inv(const InvArgs& a, dim3 grid, cudaStream_t st) {
-  const size_t smem = sizeof(inv::Smem);
-  smem_attr_once((const void*)k_inverse_core<REAL, SPIN0>, smem);
-  k_inverse_core<REAL, SPIN0><<<grid, kCoreThreadsWS, smem, st>>>(a);
+template <bool REAL, bool SPIN0, int MB>
+static void launch_inv(const InvArgs& a, int ntiles, cudaStream_t st) {
+  const size_t smem = sizeof(inv::Smem<MB>);
+  smem_attr_once((const void*)k_inverse_core<REAL, SPIN0, MB>, smem);
+  dim3 grid(ntiles, (a.nmaps + MB - 1) / MB);
+  k_inverse_core<REAL, SPIN0, MB><<<grid, kCoreThreadsWS, smem, st>>>(a);
+}
+
+template <int MB>
+static void launch_inv_mb(const InvArgs& a, int ntiles, bool real, cudaStream_t st) {
+  if (real)
+    launch_inv<true, true, MB>(a, ntiles, st);
+  else if (a.spin == 0)
+    launch_inv<false, true, MB>(a, ntiles, st);
+  else
+    launch_inv<false, false, MB>(a, ntiles, st);
 }
 
 void launch_inverse_core_paired(const InvArgs& a, int ntiles, int nmaps, bool real,
                                 cudaStream_t st);  // core_inverse_paired.cu
 
-void launch_inverse_core(const InvArgs& a, int ntiles, int nmaps, bool real, cudaStream_t st) {
-  if (a.paired) {
-    launch_inverse_core_paired(a, ntiles, nmaps, real, st);
+// Batches of two or more maps run two maps per CTA: each chain's recursion
+// then feeds both maps' contractions.
+void launch_inverse_core(const InvArgs& a0, int ntiles, int nmaps, bool real, cudaStream_t st) {
+  if (a0.paired) {
+    launch_inverse_core_paired(a0, ntiles, nmaps, real, st);
     return;
   }
-  dim3 grid(ntiles, nmaps);
-  if (real)
-    launch_inv<true, true>(a, grid, st);
-  else if (a.spin == 0)
-    launch_inv<false, true>(a, grid, st);
+  InvArgs a = a0;
+  a.nmaps = nmaps;
+  if (nmaps >= 2)
+    launch_inv_mb<2>(a, ntiles, real, st);
   else
-    launch_inv<false, false>(a, grid, st);
+    launch_inv_mb<1>(a, ntiles, real, st);
 }
 
 

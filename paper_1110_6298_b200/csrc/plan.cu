@@ -519,13 +519,17 @@ static int check_spin(mwsht_plan* p, int spin) {
 // Paired inverse tiles (core_inverse_paired.cu) cover the lower triangle
 // m' > m and emit the transposed outputs from the same chains.  Built for
 // spin 0 (complex and real), where they measured 4-11% faster than the plain
-// tiles at L = 1024-4096; spin != 0 runs the plain kernel (the paired
-// variant's extra shared-memory traffic made it slower there).
-static bool use_paired(const mwsht_plan* p, int spin) {
-  return spin == 0 && p->paired_mode != 0;
+// tiles for one map at L = 1024-4096; spin != 0 runs the plain kernel (the
+// paired variant's extra shared-memory traffic made it slower there).  Batches
+// of two or more maps run the plain kernel two maps per CTA, which shares each
+// recursion between maps instead and measured faster (C4: 12.0 vs 13.0 ms per
+// inverse of 8 maps).  mode 1 forces pairing for spin 0, mode 0 disables it.
+static bool use_paired(const mwsht_plan* p, int spin, int nmaps) {
+  if (spin != 0 || p->paired_mode == 0) return false;
+  return p->paired_mode == 1 || nmaps == 1;
 }
 
-static InvArgs inv_args(mwsht_plan* p, int spin) {
+static InvArgs inv_args(mwsht_plan* p, int spin, int nmaps = 1) {
   InvArgs a{};
   a.t = p->tabs;
   a.rowtab = p->spins[spin].rowinv;
@@ -533,7 +537,7 @@ static InvArgs inv_args(mwsht_plan* p, int spin) {
   a.colc = p->colc;
   a.gp = p->bufG;
   a.g_stride = p->strideG;
-  a.paired = use_paired(p, spin) ? 1 : 0;
+  a.paired = use_paired(p, spin, nmaps) ? 1 : 0;
   a.tiles = a.paired ? p->tiles_invp : p->tiles_inv;
   a.spin = spin;
   a.ldw = p->ldw;
@@ -630,7 +634,7 @@ static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int
   LAUNCHED(p);
   // 1. core + phases + m' mirror + theta twist (mw.py:378-402, 445)
   if (p->timing) CU(cudaEventRecord(p->ev[1][1], st));
-  InvArgs a = inv_args(p, spin);
+  InvArgs a = inv_args(p, spin, nm);
   a.out = p->bufB;
   a.out_mode = 0;
   a.out_stride = (long long)rows * N;

@@ -160,8 +160,9 @@ class Plan:
         return own.value, cf.value
 
     def set_paired(self, mode):
-        """Inverse-core tiling for spin 0: 1 or -1 (default) paired tiles (one
-        recursion feeds T[m',m] and its transpose), 0 plain tiles."""
+        """Inverse-core tiling for spin 0: -1 (default) paired tiles for single
+        maps (one recursion feeds T[m',m] and its transpose; batches share the
+        recursion between maps instead), 1 paired always, 0 plain tiles."""
         _lib.call("mwsht_plan_set_paired", self.handle, int(mode))
 
     def prepare_spin(self, spin):

@@ -262,3 +262,17 @@ def test_config5_L4096_round_trip_and_linearity(mw, O, spin):
         e0[0] = 1.0
         c = mw.inverse(mw.HarmonicCoeffs(L, 0, e0)).samples
         assert (c - 1.0 / math.sqrt(4.0 * math.pi)).abs().max().item() < 1e-14
+
+
+@pytest.mark.parametrize("L,spin,B", [(64, 0, 3), (96, -1, 5), (130, 2, 2)])
+def test_batched_maps_share_recursion(mw, O, L, spin, B):
+    # batches run two maps per CTA (one recursion, two contractions); odd batches
+    # repeat the last map in its pair without writing it
+    vals = np.stack([O.gaussian_coeffs(L, spin, 40 + k) for k in range(B)])
+    sig = mw.inverse_batch(vals, L, spin)
+    back = mw.forward_batch(sig, L, spin)
+    for b in range(B):
+        ref = O.inverse(vals[b], L, spin, threads=8)
+        assert rel(sig[b], ref) < REL_TOL
+        assert rel(back[b], O.forward(ref, L, spin, threads=8)) < REL_TOL
+        assert max_abs(back[b], vals[b]) < 1e-12
