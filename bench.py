@@ -20,8 +20,8 @@ PCG64):
   c3                       L=1024, spin 0, real path (inverse_real/forward_real)
   c4                       L=2048, spin 0, 8 maps sharded by map over ranks
   c2 / c1                  L=256 s=2 / L=64 s=0
-The default run also measures c3 and c5s2 briefly and reports them under
-"workloads".
+The default run also measures c3, c5s2 and c4 briefly and reports them
+under "workloads".
 
 --impl reference times the reference algorithm on the host CPU: the oracle/
 C restatement of the reference's numba cores (bit-identical to it) with all
@@ -580,7 +580,7 @@ def main():
     line["fp64_peak_tflops_measured"] = peak
     if not args.no_extra and args.workload == "c5s0" and ws == 1:
         extra = {}
-        for key in ("c3", "c5s2"):
+        for key in ("c3", "c5s2", "c4"):
             wk = WORKLOADS[key]
             rr = run_gpu(wk, max(3, args.steps // 2), args.warmup, rank, ws, local,
                          want_e2e=True, want_clocks=False)

@@ -1,3 +1,7 @@
+"""A/B of the batched inverse (C4: 8 maps, L=2048) with paired vs plain tiles.
+
+    python tools/batch_ab.py
+"""
 import sys, time
 sys.path.insert(0, '.')
 import numpy as np, torch
