@@ -77,7 +77,10 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
   const DevTables& T = a.t;
   const int L = T.L, N = T.N, Lp = a.ldw;
   const int2 tile = a.tiles[blockIdx.x];
-  const int r0 = tile.x, c0 = tile.y;
+  // bit 30 of tile.x: a plain tile (no transpose, every block direct) -- the
+  // longest chains at small L, where paired tiles would set the critical path
+  const bool plain_tile = (tile.x >> 30) & 1;
+  const int r0 = tile.x & 0x3fffffff, c0 = tile.y;
   const int lstart = max(r0, c0);
   const int nchunks = (L - lstart + CH - 1) / CH;
   const int lane = threadIdx.x & 31, wall = threadIdx.x >> 5;
@@ -106,7 +109,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
         if (k >= NB) mbar_wait(&sm.empty[b], ((k / NB) - 1) & 1);
         fence_proxy_async();
         uint32_t bytes = ns * (invp::R * 16u + invp::C * 8u + NG * invp::C * 16u);
-        if (PAIRED) bytes += ns * (invp::C * 8u + NG * 2u * invp::C * 16u);
+        if (PAIRED && !plain_tile) bytes += ns * (invp::C * 8u + NG * 2u * invp::C * 16u);
         mbar_arrive_expect_tx(&sm.full[b], bytes);
         auto& S = sm.st[b];
         const long long oc = blk<invp::C>(lc, c0, L);
@@ -114,7 +117,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
         bulk_g2s(&S.colc[0][0], a.colc + oc, ns * invp::C * 8, &sm.full[b]);
         bulk_g2s(&S.gp[0][0], gp + oc, ns * invp::C * 16, &sm.full[b]);
         if (!REAL) bulk_g2s(&S.gn[0][0], gn + oc, ns * invp::C * 16, &sm.full[b]);
-        if (PAIRED) {
+        if (PAIRED && !plain_tile) {
           bulk_g2s(&S.wc[0][0], a.wcol + oc, ns * invp::C * 8, &sm.full[b]);
 #pragma unroll
           for (int hh = 0; hh < 2; hh++) {
@@ -195,7 +198,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
   const int wcol_lo = PAIRED ? c0 + pc : c0 + 16 * wc;
   bool warp_has = wrow_lo < L && wcol_lo < L;
   bool mir = false;  // warp-uniform: this warp's block also emits the transpose
-  if (PAIRED) {
+  if (PAIRED && !plain_tile) {
     const int rb = r0 + 32 * h;
     if (rb < c0) warp_has = false;  // above the diagonal: produced by the mirror block
     mir = rb >= c0 + 32;

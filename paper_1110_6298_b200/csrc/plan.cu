@@ -5,6 +5,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -315,20 +316,58 @@ static int build_tiles(mwsht_plan* p) {
     for (int c0 = 0; c0 < L; c0 += kTileCols)
       inv.push_back({make_int2(r0, c0), (long long)(L - std::max(r0, c0))});
   // paired: tiles with c0 <= r0 + 32.  32x32 blocks strictly below the
-  // diagonal also produce their transpose (weight ~1.6x: the recursion is
+  // diagonal also produce their transpose (weight ~1.5x: the recursion is
   // shared), diagonal blocks run plain, blocks above the diagonal are idle.
-  for (int r0 = 0; r0 < L; r0 += kTileRows)
-    for (int c0 = 0; c0 < L && c0 <= r0 + kTileCols; c0 += kTileCols) {
-      const long long len = L - std::max(r0, c0);
-      invp.push_back({make_int2(r0, c0), c0 + kTileCols <= r0 ? (len * 8) / 5 : len});
+  // Rows below D run as plain tiles instead (tile.x bit 30, with their upper
+  // mirror tiles c0 >= r0 + 64, c0 < D): at small L one paired tile of the
+  // longest chains outlasts the per-SM share of the work.  D comes from a
+  // longest-first schedule of the weights over the SMs: the smallest D whose
+  // makespan is within 3% of the best (measured at L=1024 real: D=256 138 us,
+  // D=0 150 us; L >= 2048 gives D=0).
+  int nsm = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  auto paired_list = [&](int D) {
+    std::vector<Tl> v;
+    for (int r0 = 0; r0 < L; r0 += kTileRows)
+      for (int c0 = 0; c0 < L; c0 += kTileCols) {
+        const long long len = L - std::max(r0, c0);
+        const bool lower = c0 + kTileCols <= r0;
+        if (r0 >= D) {
+          if (c0 <= r0 + kTileCols) v.push_back({make_int2(r0, c0), lower ? (len * 3) / 2 : len});
+        } else if (c0 <= r0 + kTileCols || c0 < D) {
+          v.push_back({make_int2(r0 | (1 << 30), c0), len});
+        }
+      }
+    std::stable_sort(v.begin(), v.end(), [](const Tl& a, const Tl& b) { return a.w > b.w; });
+    return v;
+  };
+  auto makespan = [&](const std::vector<Tl>& v) {
+    std::vector<long long> load(nsm, 0);  // min-heap of SM loads
+    for (auto& x : v) {
+      std::pop_heap(load.begin(), load.end(), std::greater<long long>());
+      load.back() += x.w;
+      std::push_heap(load.begin(), load.end(), std::greater<long long>());
     }
+    return *std::max_element(load.begin(), load.end());
+  };
+  {
+    std::vector<long long> ms;
+    for (int D = 0; D < L; D += kTileRows) ms.push_back(makespan(paired_list(D)));
+    const long long best = *std::min_element(ms.begin(), ms.end());
+    int D = 0;
+    while (ms[D / kTileRows] * 100 > best * 103) D += kTileRows;
+    invp = paired_list(D);
+  }
   for (int l0 = 0; l0 < L; l0 += kTileRows) {
     const int top = std::min(l0 + kTileRows - 1, L - 1);
     for (int c0 = 0; c0 <= top; c0 += kTileCols) fwd.push_back({make_int2(l0, c0), (long long)top + 1});
   }
   auto by_work = [](const Tl& a, const Tl& b) { return a.w > b.w; };
   std::stable_sort(inv.begin(), inv.end(), by_work);
-  std::stable_sort(invp.begin(), invp.end(), by_work);
   std::stable_sort(fwd.begin(), fwd.end(), by_work);
   std::vector<int2> hi, hf, hp;
   for (auto& x : inv) hi.push_back(x.t);
