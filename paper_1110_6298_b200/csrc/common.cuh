@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <set>
 #include <utility>
@@ -277,5 +278,48 @@ inline void smem_attr_once(const void* kern, size_t bytes) {
   std::lock_guard<std::mutex> lk(mu);
   if (done.insert(std::make_pair(kern, dev)).second)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+}  // namespace mwsht
+
+// ------------------------------------------------------- programmatic dependent launch
+// The transform kernels can launch with programmatic stream serialisation: each
+// kernel triggers its dependents at entry (griddepcontrol.launch_dependents),
+// so the next kernel's CTAs start on SMs as this kernel's last wave drains and
+// run their prologue (plan tables, twiddles, chain seeds -- constant data)
+// before griddepcontrol.wait, which returns once the previous kernel has
+// completed and its memory is visible.  Every access to a mutable buffer comes
+// after the wait.  The dependents can only launch once every CTA of this grid
+// has started, so a waiting dependent never holds an SM this grid still needs.
+// Measured (bench.py, B200): C3 0.5485 -> 0.5466 ms per pair, C5 23.69 ->
+// 24.08 ms, so it is OFF by default; MWSHT_PDL=1 in the environment turns it
+// on (the kernels' griddepcontrol instructions are no-ops without it).
+namespace mwsht {
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MWSHT_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 }  // namespace mwsht

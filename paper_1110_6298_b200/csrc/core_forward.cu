@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
   constexpr int NB = Sm::NB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
+  pdl_trigger();  // dependents may start their prologue once every tile has started
   // maps of this CTA: MB * blockIdx.y + mb (the last pair of an odd batch repeats
   // its map; that copy's results are not written)
   auto map_of = [&](int mb) { return min(MB * (int)blockIdx.y + mb, a.nmaps - 1); };
@@ -91,6 +92,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
     // warpgroup 0: warp 0 streams the stages, warps 1-3 retire
     setmaxnreg_dec<kProducerRegs>();
     if (wall != 0) return;
+    pdl_wait();  // staged inputs come from the previous kernel
     // ------------------------------------------------------------ producer
     const double2* gpm[MB];
 #pragma unroll
@@ -160,6 +162,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
       sm.seedy[e][tid] = ys;
       slv |= (unsigned)lev << (4 * e);
     }
+  pdl_wait();  // the epilogue overwrites outputs the previous kernel may read
 
   double y[NE], y1[NE], acc[MB][NE][2 * NG];
 #pragma unroll
@@ -389,7 +392,7 @@ static void launch_fwd(const FwdArgs& a, int ntiles, cudaStream_t st) {
   const size_t smem = sizeof(fwd::Smem<MB>);
   smem_attr_once((const void*)k_forward_core<REAL, SPIN0, MB>, smem);
   dim3 grid(ntiles, (a.nmaps + MB - 1) / MB);
-  k_forward_core<REAL, SPIN0, MB><<<grid, kCoreThreadsWS, smem, st>>>(a);
+  launch_pdl(k_forward_core<REAL, SPIN0, MB>, grid, dim3(kCoreThreadsWS), smem, st, a);
 }
 
 template <int MB>

@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
   constexpr int NB = Sm::NB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
+  pdl_trigger();  // dependents may start their prologue once every tile has started
   // maps of this CTA: MB * blockIdx.y + mb (the last pair of an odd batch repeats
   // its map; that copy's results are not written)
   auto map_of = [&](int mb) { return min(MB * (int)blockIdx.y + mb, a.nmaps - 1); };
@@ -94,6 +95,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
     // warpgroup 0: warp 0 streams the stages, warps 1-3 retire; registers go to the consumers
     setmaxnreg_dec<kProducerRegs>();
     if (wall != 0) return;
+    pdl_wait();  // staged inputs come from the previous kernel
     // ------------------------------------------------------------ producer
     const double2* rowtab = a.rowtab;
     const double2* gpm[MB];
@@ -164,6 +166,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
       sm.seedz[e][tid] = zs;
       slv |= (unsigned)lev << (4 * e);
     }
+  pdl_wait();  // the epilogue overwrites outputs the previous kernel may read
 
   double z[NE], zp[NE], acc[MB][NE][2 * NG];
 #pragma unroll
@@ -409,7 +412,7 @@ static void launch_inv(const InvArgs& a, int ntiles, cudaStream_t st) {
   const size_t smem = sizeof(inv::Smem<MB>);
   smem_attr_once((const void*)k_inverse_core<REAL, SPIN0, MB>, smem);
   dim3 grid(ntiles, (a.nmaps + MB - 1) / MB);
-  k_inverse_core<REAL, SPIN0, MB><<<grid, kCoreThreadsWS, smem, st>>>(a);
+  launch_pdl(k_inverse_core<REAL, SPIN0, MB>, grid, dim3(kCoreThreadsWS), smem, st, a);
 }
 
 template <int MB>

@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
   using Sm = invp::Smem<CH, PAIRED>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
+  pdl_trigger();  // dependents may start their prologue once every tile has started
 
   const DevTables& T = a.t;
   const int L = T.L, N = T.N, Lp = a.ldw;
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
     // warpgroup 0: warp 0 streams the stages, warps 1-3 retire; registers go to the consumers
     setmaxnreg_dec<kProducerRegs>();
     if (wall != 0) return;
+    pdl_wait();  // staged inputs come from the previous kernel
     // ------------------------------------------------------------ producer
     const double2* rowtab = a.rowtab;
     const double2* gp = a.gp + (long long)blockIdx.y * a.g_stride;
@@ -179,6 +181,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
       sm.seedz[e][tid] = zs;
       slv |= (unsigned)lev << (4 * e);
     }
+  pdl_wait();  // the epilogue overwrites outputs the previous kernel may read
 
   double z[NE], zp[NE], acc[NE][2 * NG], acm[NA][2 * NG];
 #pragma unroll
@@ -456,7 +459,7 @@ template <bool REAL, bool SPIN0, bool PAIRED>
 static void launch_inv_paired(const InvArgs& a, dim3 grid, cudaStream_t st) {
   const size_t smem = sizeof(invp::Smem<PAIRED ? 8 : kChunk, PAIRED>);
   smem_attr_once((const void*)k_inverse_core_paired<REAL, SPIN0, PAIRED>, smem);
-  k_inverse_core_paired<REAL, SPIN0, PAIRED><<<grid, kCoreThreadsWS, smem, st>>>(a);
+  launch_pdl(k_inverse_core_paired<REAL, SPIN0, PAIRED>, grid, dim3(kCoreThreadsWS), smem, st, a);
 }
 
 void launch_inverse_core_paired(const InvArgs& a, int ntiles, int nmaps, bool real,

@@ -358,12 +358,14 @@ __device__ __forceinline__ void bluestein(double2* X, const double2* tw, double2
 
 // Per-CTA setup shared by the stage kernels: team split, buffers, twiddles.
 #define FFT_PROLOGUE                                                         \
+  pdl_trigger();                                                             \
   using C = Cfg<LOGH>;                                                       \
   extern __shared__ __align__(16) double2 sm[];                              \
   const int team = threadIdx.x / C::TEAM, lt = threadIdx.x - team * C::TEAM; \
   double2* X = sm + team * C::H;                                             \
   double2* tws = sm + C::NR * C::H;                                          \
   load_tw(tws, a);                                                           \
+  pdl_wait(); /* every access below touches the previous stage's output */   \
   double2* scr = a.scratch + ((long long)blockIdx.x * C::NR + team) * 3 * C::H;
 
 // ------------------------------------------------------------------ kernels
@@ -712,7 +714,7 @@ static void launch_t(K kern, const FftArgs& a, int nsm, cudaStream_t st) {
   long long grid = (rows + C::NR - 1) / C::NR;
   if (grid > nsm) grid = nsm;
   if (grid < 1) grid = 1;
-  kern<<<(int)grid, kT, sm, st>>>(a);
+  launch_pdl(kern, dim3((unsigned)grid), dim3(kT), sm, st, a);
 }
 
 template <int LOGH>

@@ -165,6 +165,8 @@ __global__ void k_inv_prescale(const double2* __restrict__ in, int in_mode,
                                const double* __restrict__ cl, const double* __restrict__ A, int L,
                                int ldw, double2* __restrict__ gp, long long in_stride,
                                long long g_stride) {
+  pdl_trigger();
+  pdl_wait();  // reads the caller's coefficients, overwrites the core staging
   const int l = blockIdx.y;
   const int N = 2 * L - 1;
   const double2* f = in + (long long)blockIdx.z * in_stride;
@@ -332,9 +334,9 @@ void launch_inv_prescale(bool real, const double2* in, int in_mode, const double
   const int threads = 128;
   dim3 grid((ldw + threads - 1) / threads, L, nm);
   if (real)
-    k_inv_prescale<true><<<grid, threads, 0, st>>>(in, in_mode, cl, A, L, ldw, gp, is, gs);
+    launch_pdl(k_inv_prescale<true>, grid, threads, 0, st, in, in_mode, cl, A, L, ldw, gp, is, gs);
   else
-    k_inv_prescale<false><<<grid, threads, 0, st>>>(in, in_mode, cl, A, L, ldw, gp, is, gs);
+    launch_pdl(k_inv_prescale<false>, grid, threads, 0, st, in, in_mode, cl, A, L, ldw, gp, is, gs);
 }
 
 void launch_transpose(const double2* in, double2* out, int rows, int cols, cudaStream_t st) {
