@@ -525,8 +525,8 @@ def summarize(key, wl, r, ws, peak_tf, steps, warmup, with_cpu, cpu_budget):
     if "e2e_total_ms" in r:
         line["e2e"] = {"value": pairs / (r["e2e_total_ms"] / 1e3), "unit": "fwd+inv pairs/s",
                        "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
-                       "path": "paper_1110_6298_b200.inverse/forward (public API), pinned host "
-                               "buffers", "max_abs_err": r["e2e_err"]}
+                       "path": "paper_1110_6298_b200.pipeline.HostPipeline (public API; "
+                               "inverse/forward or the *_real pair per map), pinned host buffers", "max_abs_err": r["e2e_err"]}
     if with_cpu:
         v, sample, cores = cpu_reference(wl, budget_s=cpu_budget)
         line["cpu_baseline"] = {"value": v, "unit": "fwd+inv pairs/s", "cores": cores,

@@ -108,6 +108,13 @@ int mwsht_inverse_real_d(mwsht_plan *plan, const void *flm, double *samples, int
 int mwsht_reality_residual(mwsht_plan *plan, const void *flm, double *worst_host,
                            double *tol_host, void *stream);
 
+/* The same check without a host sync (pipelined callers, which report the
+ * violation later): max-reduces the residual and max|f| into
+ * dev_worst_peak[0..1] (device memory, float64 bit patterns as uint64,
+ * zero-initialised by the caller); tolerance = 1e-12 max(1, peak). */
+int mwsht_reality_residual_async(mwsht_plan *plan, const void *flm,
+                                 unsigned long long *dev_worst_peak, void *stream);
+
 /* Batched transforms over `nmaps` independent maps laid out back to back
  * (map stride L*L for coefficients, L*N for samples); nmaps <= max_batch.
  * Same per-map semantics as the single-map calls (the callers'

@@ -45,6 +45,7 @@ _SIGS = {
     "mwsht_inverse_real_d": ([_P, _P, _P, _I, _P], _I),
     "mwsht_reality_residual": ([_P, _P, ctypes.POINTER(ctypes.c_double),
                                 ctypes.POINTER(ctypes.c_double), _P], _I),
+    "mwsht_reality_residual_async": ([_P, _P, _P, _P], _I),
     "mwsht_forward_z_batch": ([_P, _I, _P, _P, _I, _I, _P], _I),
     "mwsht_inverse_z_batch": ([_P, _I, _P, _P, _I, _I, _P], _I),
     "mwsht_fmm_core": ([_P, _P, _P, _I, _I, _P, _P], _I),

@@ -853,6 +853,16 @@ int mwsht_reality_residual(mwsht_plan* p, const void* flm, double* worst_host, d
   return MWSHT_OK;
 }
 
+int mwsht_reality_residual_async(mwsht_plan* p, const void* flm, unsigned long long* dev_worst_peak,
+                                 void* stream) {
+  int rc;
+  if ((rc = check_plan(p))) return rc;
+  if (!dev_worst_peak) return fail(MWSHT_E_CONTRACT, "reality_residual_async", "null result buffer");
+  launch_reality((const double2*)flm, p->L, dev_worst_peak, nullptr, (cudaStream_t)stream);
+  CU(cudaGetLastError());
+  return MWSHT_OK;
+}
+
 int mwsht_fmm_core(mwsht_plan* p, const void* flm2d, const double* cl, int spin, int use_trapani,
                    void* T, void* stream) {
   int rc;

@@ -371,7 +371,7 @@ void launch_reality(const double2* f, int L, unsigned long long* red, unsigned l
   long long blocks = (n + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   k_reality<<<(unsigned)blocks, 256, 0, st>>>(f, L, red, red + 1);
-  k_reality_publish<<<1, 1, 0, st>>>(red, host);
+  if (host) k_reality_publish<<<1, 1, 0, st>>>(red, host);
 }
 
 }  // namespace mwsht

@@ -346,12 +346,19 @@ def inverse_real(coeffs, recursion="trapani"):
     if worst > tol:
         raise SymmetryError(
             f"coefficients violate the reality condition by {worst:.3e} (tolerance {tol:.3e})")
+    out = _inverse_real_unchecked(f, L, recursion)
+    return _trusted(MwSignal, L, 0, _back(out, coeffs.values))
+
+
+def _inverse_real_unchecked(f, L, recursion):
+    """inverse_real's transform on a device tensor whose reality condition the
+    caller checks (HostPipeline defers it to synchronize())."""
     dev = f.device.index
     out = torch.empty((L, 2 * L - 1), dtype=torch.float64, device=f"cuda:{dev}")
     plan = get_plan(L, dev)
     _lib.call("mwsht_inverse_real_d", plan.handle, f.data_ptr(), out.data_ptr(),
               _REC_ID[recursion], _stream(dev))
-    return _trusted(MwSignal, L, 0, _back(out, coeffs.values))
+    return out
 
 
 # ------------------------------------------------------------- batches

@@ -24,11 +24,20 @@ and nothing overlaps.
 
 The results in ``h_out`` are valid after ``synchronize()``, or after ``join()``
 followed by a sync of the caller's stream.
+
+The real path's reality check (``inverse_real`` raises ``SymmetryError``,
+mw.py:537-547) needs a device reduction; ``inverse_real`` waits for it, which
+would stall the pipeline every map.  The pipeline instead reduces each map's
+residual into its own device slot and checks the slots in ``synchronize()``,
+which raises ``SymmetryError`` naming the offending submissions.  A violating
+map's output is still computed (like every other map in flight).
 """
+
+import struct
 
 import torch
 
-from . import mw
+from . import _lib, mw
 
 KINDS = ("inverse", "forward", "roundtrip")
 
@@ -62,16 +71,29 @@ class HostPipeline:
         self.slots = [dict(buf=torch.empty(shape, dtype=dtype, device=dev),
                            loaded=torch.cuda.Event(), consumed=None) for _ in range(depth)]
         self.k = 0
-        mw.get_plan(L, self.device)
+        self.pending = []  # (submission index, device (2,) uint64 worst/peak) of real inverses
+        self.plan = mw.get_plan(L, self.device)
 
     def _run(self, x):
         L, s, rec = self.L, self.spin, self.recursion
         if self.kind in ("inverse", "roundtrip"):
             # the l < |spin| zeros were checked on the host copy in submit()
-            c = mw._trusted(mw.HarmonicCoeffs, L, s, x, lead_checked=True)
-            sig = mw.inverse_real(c, rec) if self.real else mw.inverse(c, rec)
-            if self.kind == "inverse":
-                return sig.samples
+            if self.real:
+                # deferred reality check (see the module docstring)
+                red = torch.zeros(2, dtype=torch.int64, device=x.device)
+                _lib.call("mwsht_reality_residual_async", self.plan.handle, x.data_ptr(),
+                          red.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream)
+                self.pending.append((self.k - 1, red))
+                mw._check_recursion(rec)
+                samples = mw._inverse_real_unchecked(x, L, rec)
+                if self.kind == "inverse":
+                    return samples
+                sig = mw._trusted(mw.MwSignal, L, 0, samples)
+            else:
+                c = mw._trusted(mw.HarmonicCoeffs, L, s, x, lead_checked=True)
+                sig = mw.inverse(c, rec)
+                if self.kind == "inverse":
+                    return sig.samples
         else:
             sig = mw.MwSignal(L, s, x)
         out = mw.forward_real(sig, rec) if self.real else mw.forward(sig, rec)
@@ -123,3 +145,16 @@ class HostPipeline:
     def synchronize(self):
         self.join()
         torch.cuda.current_stream(self.device).synchronize()
+        self._check_reality()
+
+    def _check_reality(self):
+        pending, self.pending = self.pending, []
+        bad = []
+        for k, red in pending:
+            w, pk = (struct.unpack("<d", struct.pack("<q", int(v)))[0] for v in red.tolist())
+            tol = 1e-12 * max(1.0, pk)
+            if w > tol:
+                bad.append(f"submission {k}: residual {w:.3e} > tolerance {tol:.3e}")
+        if bad:
+            from .errors import SymmetryError
+            raise SymmetryError("coefficients violate the reality condition: " + "; ".join(bad))

@@ -59,3 +59,27 @@ def test_pipeline_rejects_low_degree_for_spin():
     bad[1] = 1.0
     with pytest.raises(mw.ContractViolationError):
         pipe.submit(bad, torch.empty((L, 2 * L - 1), dtype=torch.complex128))
+
+
+def test_pipeline_defers_reality_check_to_synchronize():
+    # inverse_real raises SymmetryError for a non-real coefficient set (mw.py:537-547);
+    # the pipeline reports it at synchronize() and names the submission
+    import torch
+    from oracle import mw_oracle as O
+    import paper_1110_6298_b200 as mw
+    from paper_1110_6298_b200.pipeline import HostPipeline
+    L = 24
+    good = torch.from_numpy(O.gaussian_real_coeffs(L, 3)).pin_memory()
+    bad = torch.from_numpy(O.gaussian_coeffs(L, 0, 4)).pin_memory()
+    outs = [torch.empty((L, 2 * L - 1), dtype=torch.float64).pin_memory() for _ in range(3)]
+    pipe = HostPipeline(L, 0, kind="inverse", real=True, device=0, depth=2)
+    pipe.submit(good, outs[0])
+    pipe.submit(bad, outs[1])
+    pipe.submit(good, outs[2])
+    with pytest.raises(mw.SymmetryError, match="submission 1"):
+        pipe.synchronize()
+    ref = mw.inverse_real(mw.HarmonicCoeffs(L, 0, good.numpy().copy())).samples
+    assert np.max(np.abs(outs[0].numpy() - ref)) == 0.0
+    assert np.max(np.abs(outs[2].numpy() - ref)) == 0.0
+    pipe.submit(good, outs[0])
+    pipe.synchronize()  # the error was reported once; the pipeline keeps working
