@@ -12,12 +12,14 @@ from .errors import (ContractViolationError, ConvergenceError, DeviceError,
 from .mw import (HarmonicCoeffs, MwSignal, Plan, check_band_limit, clear_plans, forward,
                  forward_batch, forward_real, get_plan, inverse, inverse_batch, inverse_real,
                  mw_grid_phis, mw_grid_thetas, reality_residual)
+from .io import load_coeffs, load_signal, read_coeffs_to, read_signal_to, save_coeffs, save_signal
 from .pipeline import HostPipeline
 
 __all__ = [
     "HarmonicCoeffs", "MwSignal", "forward", "inverse", "forward_real", "inverse_real",
     "forward_batch", "inverse_batch", "reality_residual", "HostPipeline", "check_band_limit",
     "mw_grid_thetas", "mw_grid_phis", "Plan", "get_plan", "clear_plans",
+    "save_coeffs", "load_coeffs", "save_signal", "load_signal", "read_coeffs_to", "read_signal_to",
     "TorushtError", "InvalidBandLimitError", "InvalidSpinError", "ContractViolationError",
     "UnsupportedDegreeError", "SymmetryError", "ConvergenceError", "DeviceError",
 ]
