@@ -367,6 +367,41 @@ def inverse_real(values, L, recursion="trapani", threads=None):
     return np.fft.irfft(rows.T, n=2 * L - 1, axis=1, norm="forward")
 
 
+# ------------------------------------------- reduced grid, quadrature -----
+
+def synthesize_reduced(values, L, spin, recursion="trapani", threads=None):
+    """mw.py:449-466: samples on the reduced (L, L) grid (theta_t, 2 pi p/L):
+    theta synthesis, orders folded by residue mod L, an L-point inverse DFT."""
+    F = fourier_plane_inverse(values, L, spin, recursion, threads)
+    rows = theta_synthesis(F, L)[:, :L]                   # (N orders, L rings)
+    m = np.arange(-(L - 1), L)
+    bins = np.zeros((L, L), dtype=np.complex128)
+    np.add.at(bins, m % L, rows)
+    return (np.fft.ifft(bins, axis=0) * L).T.copy()
+
+
+def ring_weights_v(L):
+    """quadrature.py:77-93: v(theta_t) = (1/N) sum_{|m'|<L} w(-m') e^{i m' theta_t}."""
+    mp = np.arange(-(L - 1), L)
+    theta0 = math.pi / (2 * L - 1)
+    spectrum = weights_w(-mp) * np.exp(1j * mp * theta0)
+    return np.fft.ifft(np.fft.ifftshift(spectrum))
+
+
+def quad_weights_q(L, spin):
+    """quadrature.py:96-111: q(theta_t) = 2pi/L [v(theta_t) + (-1)^s v(theta_{2L-2-t})]."""
+    v = ring_weights_v(L)
+    q = v[:L].copy()
+    if L > 1:
+        q[: L - 1] += (-1.0 if spin % 2 else 1.0) * v[2 * L - 2: L - 1: -1]
+    return q * (2.0 * math.pi / L)
+
+
+def integrate(samples, q):
+    """quadrature.py:123-139: sum_t q_t sum_p f[t, p] on the reduced grid."""
+    return complex(np.sum(np.asarray(samples).sum(axis=1) * q))
+
+
 # ------------------------------------------------------------ inputs -----
 
 def gaussian_coeffs(L, spin, seed):

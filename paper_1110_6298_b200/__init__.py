@@ -14,11 +14,15 @@ from .mw import (HarmonicCoeffs, MwSignal, Plan, check_band_limit, clear_plans, 
                  mw_grid_phis, mw_grid_thetas, reality_residual)
 from .io import load_coeffs, load_signal, read_coeffs_to, read_signal_to, save_coeffs, save_signal
 from .pipeline import HostPipeline
+from .quadrature import (QuadWeights, integrate, quad_weights, quad_weights_q, ring_weights_v,
+                         synthesize_reduced, weight_w)
 
 __all__ = [
     "HarmonicCoeffs", "MwSignal", "forward", "inverse", "forward_real", "inverse_real",
     "forward_batch", "inverse_batch", "reality_residual", "HostPipeline", "check_band_limit",
     "mw_grid_thetas", "mw_grid_phis", "Plan", "get_plan", "clear_plans",
+    "synthesize_reduced", "quad_weights", "quad_weights_q", "ring_weights_v", "weight_w",
+    "integrate", "QuadWeights",
     "save_coeffs", "load_coeffs", "save_signal", "load_signal", "read_coeffs_to", "read_signal_to",
     "TorushtError", "InvalidBandLimitError", "InvalidSpinError", "ContractViolationError",
     "UnsupportedDegreeError", "SymmetryError", "ConvergenceError", "DeviceError",

@@ -95,3 +95,17 @@ def test_real_coefficients_are_real_symmetric():
     v = O.gaussian_real_coeffs(12, 3)
     worst, tol = O.reality_residual(v, 12)
     assert worst <= tol
+
+
+@pytest.mark.parametrize("L,s", [(1, 0), (2, 1), (7, 0), (16, -2), (33, 3), (64, 0)])
+def test_oracle_reduced_grid_and_quadrature_match_reference(L, s):
+    import os
+    from conftest import ROOT
+    g = np.load(os.path.join(ROOT, "tests", "golden", "reduced.npz"))
+    v = O.gaussian_coeffs(L, s, 100 + L)
+    key = f"L{L}_s{s}"
+    assert np.max(np.abs(O.synthesize_reduced(v, L, s) - g[key + "_reduced"])) == 0.0
+    assert np.max(np.abs(O.ring_weights_v(L) - g[key + "_v"])) == 0.0
+    q = O.quad_weights_q(L, s)
+    assert np.max(np.abs(q - g[key + "_q"])) == 0.0
+    assert O.integrate(g[key + "_reduced"], q) == complex(g[key + "_integral"])
