@@ -562,7 +562,7 @@ def main():
                                            "% of FP64/HBM roofline",
             "value": value, "unit": "fwd+inv pairs/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "strong" if wl["shard"] == "maps" else "weak",
+            "scaling": "strong" if wl["shard"] in ("maps", "mcolumn") else "weak",
             "vs_baseline": None, "dtype": "f64 (complex128)",
             "data": "synthetic: seeded N(0,1) coefficients (PCG64), BASELINE.json configs",
             "config": {"workload": wl["name"], "L": wl["L"], "spin": wl["spin"],
