@@ -64,6 +64,9 @@ __device__ __forceinline__ void rescale_p(double (&z)[NE], double (&zp)[NE], uns
 
 template <bool REAL, bool SPIN0, bool PAIRED>
 __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvArgs a) {
+  // Built for spin 0 only (plan.cu use_paired); the SPIN0 / PAIRED template
+  // parameters keep the general control flow readable next to core_inverse.cu.
+  static_assert(SPIN0 && PAIRED, "paired tiles are instantiated for spin 0 only");
   constexpr int CH = PAIRED ? 8 : kChunk;  // degrees per stage (paired stages carry 2x data)
   constexpr int NB = kStages;
   constexpr int NI = 4, NJ = 2, NE = NI * NJ;
