@@ -276,3 +276,20 @@ def test_batched_maps_share_recursion(mw, O, L, spin, B):
         assert rel(sig[b], ref) < REL_TOL
         assert rel(back[b], O.forward(ref, L, spin, threads=8)) < REL_TOL
         assert max_abs(back[b], vals[b]) < 1e-12
+
+
+def test_bitwise_repeatable(mw, O):
+    # SPEC.md:293 (fixed summation order): the same input gives the same bits,
+    # which also rules out shared-memory races in the TMA/mbarrier rings
+    for L, s, real in [(300, 0, False), (257, 3, False), (200, 0, True)]:
+        v = O.gaussian_real_coeffs(L, 5) if real else O.gaussian_coeffs(L, s, 5)
+        inv = mw.inverse_real if real else mw.inverse
+        fwd = mw.forward_real if real else mw.forward
+        a = inv(mw.HarmonicCoeffs(L, s, v.copy())).samples
+        b = inv(mw.HarmonicCoeffs(L, s, v.copy())).samples
+        assert np.array_equal(a, b)
+        fa = fwd(mw.MwSignal(L, s, np.array(a))).values
+        fb = fwd(mw.MwSignal(L, s, np.array(a))).values
+        assert np.array_equal(fa, fb)
+    vals = np.stack([O.gaussian_coeffs(160, 0, k) for k in range(3)])
+    assert np.array_equal(mw.inverse_batch(vals, 160, 0), mw.inverse_batch(vals, 160, 0))
