@@ -293,3 +293,15 @@ def test_bitwise_repeatable(mw, O):
         assert np.array_equal(fa, fb)
     vals = np.stack([O.gaussian_coeffs(160, 0, k) for k in range(3)])
     assert np.array_equal(mw.inverse_batch(vals, 160, 0), mw.inverse_batch(vals, 160, 0))
+
+
+@pytest.mark.parametrize("L", [1, 2, 3, 33, 101])
+def test_real_path_odd_and_tiny_band_limits(mw, O, L):
+    # two rings / two order rows per transform: odd counts leave a single one
+    v = O.gaussian_real_coeffs(L, L)
+    sig = mw.inverse_real(mw.HarmonicCoeffs(L, 0, v.copy())).samples
+    ref = O.inverse_real(v, L)
+    assert max_abs(sig, ref) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+    back = mw.forward_real(mw.MwSignal(L, 0, np.array(sig))).values
+    assert max_abs(back, O.forward_real(ref, L)) < 1e-12 * max(1.0, np.max(np.abs(v)))
+    assert max_abs(back, v) < 1e-12 * max(1.0, np.max(np.abs(v)))
