@@ -15,7 +15,10 @@
 // one on l = m mod 2).  The two warps on an SMSP run the same (row, column)
 // parity code path, and full chunks run as a rolled loop over degree pairs:
 // four such bodies are live per CTA and an unrolled chunk per body overflowed
-// the instruction cache (ncu: no_instruction stalls, 2x slower).
+// the instruction cache (ncu: no_instruction stalls, 2x slower).  Stages hold
+// 16 degrees (3 x 72 KB); the chain seeds are recomputed at the ghost start
+// instead of parked in shared memory (8 -> 16 degrees per stage: 7.64 ->
+// 7.22 ms at L=4096).
 #include "common.cuh"
 
 #ifndef MWSHT_PAIR_UNROLL
@@ -42,9 +45,9 @@ struct Stage {
 };
 template <int CH, bool P>
 struct Smem {
-  Stage<CH, P> st[kStages];
-  double seedz[8][kConsumerThreads];
-  uint64_t full[kStages], empty[kStages];
+  static constexpr int NB = 3;  // 3 x 72 KB stages of 16 degrees (no seed buffer: see ghost start)
+  Stage<CH, P> st[NB];
+  uint64_t full[NB], empty[NB];
 };
 }  // namespace invp
 
@@ -67,8 +70,8 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
   // Built for spin 0 only (plan.cu use_paired); the SPIN0 / PAIRED template
   // parameters keep the general control flow readable next to core_inverse.cu.
   static_assert(SPIN0 && PAIRED, "paired tiles are instantiated for spin 0 only");
-  constexpr int CH = PAIRED ? 8 : kChunk;  // degrees per stage (paired stages carry 2x data)
-  constexpr int NB = kStages;
+  constexpr int CH = kChunk;  // degrees per stage
+  constexpr int NB = invp::Smem<CH, PAIRED>::NB;
   constexpr int NI = 4, NJ = 2, NE = NI * NJ;
   constexpr int NG = REAL ? 1 : 2;     // complex g values per column: f_{l,m} (+ f_{l,-m})
   constexpr int CJ = PAIRED ? 16 : 8;  // column distance between a thread's chains
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
 
   // -------------------------------------------------------------- consumers
   setmaxnreg_inc<kConsumerRegs>();
-  const int w = wall - 4, tid = threadIdx.x - 128;
+  const int w = wall - 4;
   double2* __restrict__ out = a.out + (long long)blockIdx.y * a.out_stride;
   // Warps w and w+4 share an SMSP (warp id mod 4).  Plain: (par, h) = bits of w & 3,
   // wc = w >> 2.  Paired: the SMSP's two warps run the same (par, pc) code path
@@ -164,26 +167,18 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
 
   // seeds: z^{l0} = Delta^{l0}_{m'm} / ((-1)^l0 lam_l0 u_l0(m) u_l0(m')), l0 = max(m', m),
   // Delta^{l0}_{m'm} = sign sqrt(C(2 l0, l0 + min))/2^l0 = sign P0(l0) R(l0+mu) R(l0-mu)
-  // (common.cuh seed factors), carried in exponent levels
-  unsigned slv = 0;  // seed levels, 4 bits per chain
-#pragma unroll
-  for (int i = 0; i < NI; i++)
-#pragma unroll
-    for (int j = 0; j < NJ; j++) {
-      const int e = i * NJ + j;
-      double zs = 0.0;
-      int lev = 0;
-      if (mp[i] < L && mm[j] < L) {
-        const int l0 = max(mp[i], mm[j]), mu = min(mp[i], mm[j]);
-        int ex;
-        double s_ = seed3(T.sd_pi[l0], T.sd_qi[l0 + mu], T.sd_qi[l0 - mu], ex);
-        if (mm[j] < mp[i] && ((mp[i] - mm[j]) & 1)) s_ = -s_;
-        if (l0 & 1) s_ = -s_;
-        zs = split_level(s_, ex, lev);
-      }
-      sm.seedz[e][tid] = zs;
-      slv |= (unsigned)lev << (4 * e);
-    }
+  // (common.cuh seed factors), carried in exponent levels; computed at the
+  // ghost start from the constant factor tables (no shared-memory buffer)
+  auto seed_of = [&](int i, int j, int& lev) {
+    lev = 0;
+    if (mp[i] >= L || mm[j] >= L) return 0.0;
+    const int l0 = max(mp[i], mm[j]), mu = min(mp[i], mm[j]);
+    int ex;
+    double s_ = seed3(T.sd_pi[l0], T.sd_qi[l0 + mu], T.sd_qi[l0 - mu], ex);
+    if (mm[j] < mp[i] && ((mp[i] - mm[j]) & 1)) s_ = -s_;
+    if (l0 & 1) s_ = -s_;
+    return split_level(s_, ex, lev);
+  };
   pdl_wait();  // the epilogue overwrites outputs the previous kernel may read
 
   double z[NE], zp[NE], acc[NE][2 * NG], acm[NA][2 * NG];
@@ -288,13 +283,16 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
       if (!started) {
         // Ghost start: see core_inverse.cu.  The transposed contraction's
         // ghost terms meet W_l(m) or g_l(m'), likewise exactly 0 below l0.
+        unsigned slv = 0;  // seed levels, 4 bits per chain
 #pragma unroll
         for (int i = 0; i < NI; i++)
 #pragma unroll
           for (int j = 0; j < NJ; j++) {
             const int e = i * NJ + j;
             const int d = max(mp[i], mm[j]) - lc;  // >= 0: lc <= wl0_min <= l0
-            const double sd = (mp[i] < L && mm[j] < L) ? sm.seedz[e][tid] : 0.0;
+            int lev;
+            const double sd = seed_of(i, j, lev);
+            slv |= (unsigned)lev << (4 * e);
             const double g0 = ((d >> 1) & 1) ? -sd : sd;        // z^{lc}   (d even)
             const double g1 = (((d + 1) >> 1) & 1) ? -sd : sd;  // z^{lc-1} (d odd)
             z[e] = (d & 1) ? 0.0 : g0;
@@ -460,7 +458,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
 
 template <bool REAL, bool SPIN0, bool PAIRED>
 static void launch_inv_paired(const InvArgs& a, dim3 grid, cudaStream_t st) {
-  const size_t smem = sizeof(invp::Smem<PAIRED ? 8 : kChunk, PAIRED>);
+  const size_t smem = sizeof(invp::Smem<kChunk, PAIRED>);
   smem_attr_once((const void*)k_inverse_core_paired<REAL, SPIN0, PAIRED>, smem);
   launch_pdl(k_inverse_core_paired<REAL, SPIN0, PAIRED>, grid, dim3(kCoreThreadsWS), smem, st, a);
 }
