@@ -24,7 +24,17 @@
 // which feeds two contractions from one recursion via the transpose symmetry.
 #include "common.cuh"
 
+#ifndef MWSHT_INV_UNROLL
+// degree pairs per loop iteration (spin 0) for two-map CTAs; one-map CTAs
+// unroll the whole chunk.  C4 (8 maps, L=2048): 2 -> 11.36 ms per inverse
+// batch, 4 -> 12.15, 8 -> 12.08.
+#define MWSHT_INV_UNROLL 2
+#endif
+#ifndef MWSHT_NS_UNROLL
+#define MWSHT_NS_UNROLL 16  // degrees per loop iteration (spin != 0): full chunk measured best
+#endif
 namespace mwsht {
+constexpr int INV_UNR = MWSHT_INV_UNROLL, NS_UNR = MWSHT_NS_UNROLL;
 
 
 namespace inv {
@@ -296,20 +306,20 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
             if (SPIN0) {
               // lc is even (tile corners are multiples of 32): pairs (even l, odd l)
               if (par == 0) {
-#pragma unroll
+#pragma unroll(MB == 2 ? INV_UNR : kChunk / 2)
                 for (int s = 0; s < kChunk; s += 2) {
                   full_step(masked, s);
                   rec_step(s + 1);
                 }
               } else {
-#pragma unroll
+#pragma unroll(MB == 2 ? INV_UNR : kChunk / 2)
                 for (int s = 0; s < kChunk; s += 2) {
                   rec_step(s);
                   full_step(masked, s + 1);
                 }
               }
             } else {
-#pragma unroll
+#pragma unroll NS_UNR
               for (int s = 0; s < kChunk; s++) full_step(masked, s);
             }
           } else if (SPIN0) {
