@@ -460,11 +460,16 @@ __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
   double2* scrF[2] = {scr + C::H, scr + 2 * C::H};  // F of the task's rows (N <= H)
   const int L = a.L, N = a.N, ldw = a.ldw;
   constexpr int H = C::H, M = C::M;
-  const int ntask = theta_tasks(a.m0, a.m1, REAL);
+  // Two rows per transform from H = 2048 (L >= 1024) on, where the rows
+  // outnumber the teams; below, every row gets its own team in one wave and
+  // the shorter unpaired task (4 instead of 6 half-convolutions) wins
+  // (L=64: 79 -> 46 us, L=256: 128 -> 74 us per launch).
+  constexpr bool PAIR = LOGH >= 11;
+  const int ntask = PAIR ? theta_tasks(a.m0, a.m1, REAL) : a.nrows;
   for (int task = blockIdx.x * C::NR + team; task < ntask * a.nmaps; task += gridDim.x * C::NR) {
     const int map = task / ntask, q = task - map * ntask;
-    int i1;
-    const bool two = theta_task(q, a.m0, a.m1, REAL, i1) == 2;
+    int i1 = q;
+    const bool two = PAIR && theta_task(q, a.m0, a.m1, REAL, i1) == 2;
     int mr[2];
     double eps[2];
     const double2* g[2];
@@ -476,7 +481,7 @@ __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
     }
     // 1. Bluestein DFT_N of the periodic extension(s): X[k] = M Z[k]
     auto ext = [&](int u, int n) { return n < L ? g[u][n] : cscale(g[u][2 * L - 2 - n], eps[u]); };
-    bluestein<LOGH, false, true>(
+    bluestein<LOGH, false, PAIR>(
         X, tws, scr, a, lt, team,
         [&](int n) {
           const double2 x1 = ext(0, n);
@@ -539,11 +544,11 @@ __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
         if (p >= M - L + 1) return F[p - M + N];
         return make_double2(0.0, 0.0);
       };
-      conv_half<LOGH, true>(
+      conv_half<LOGH, PAIR>(
           X, tws, a.specw + H, lt, team,
           [&](int j) { return cmul(csub(Fpl(j), Fpl(j + H)), omega(tws, j, M)); },
           [&](int k, double2 v) { scr[k] = v; });
-      conv_half<LOGH, true>(
+      conv_half<LOGH, PAIR>(
           X, tws, a.specw, lt, team, [&](int j) { return cadd(Fpl(j), Fpl(j + H)); },
           [&](int k, double2 v) { X[phys(k)] = v; });
       team_sync<C::TEAM>(team);
