@@ -21,8 +21,16 @@
  *   - All data pointers are DEVICE pointers on the plan's device unless the
  *     name says _host.  Inputs are read-only; outputs are fully overwritten.
  *   - `stream` is a cudaStream_t (0 = legacy default stream).  Calls are
- *     asynchronous with respect to the host except where noted; one plan may
- *     be used from one stream at a time (plans own scratch buffers).
+ *     asynchronous with respect to the host except where noted.  A plan owns
+ *     scratch buffers; calls on one plan from several threads and streams are
+ *     safe (reentrant): the host side is serialised by a mutex and
+ *     on the device each call waits for the previous call's work on another
+ *     stream (an event hand-off), so concurrent callers never share scratch
+ *     in flight.
+ *   - Every entry point restores the caller's current CUDA device.
+ *   - Band limits: every L >= 1 up to the documented cap L <= 4096 (the FFT
+ *     engine keeps one M/2-point half-convolution in an SM's shared memory);
+ *     larger L fails with MWSHT_E_DEGREE (UnsupportedDegreeError).
  *   - `recursion`: MWSHT_TRAPANI or MWSHT_RISBO.  Both are accepted for
  *     drop-in compatibility (mw.py:43,562-566); both run the same stable GPU
  *     recursions (inverse: l-recursion, forward: exponent-scaled Trapani
@@ -50,7 +58,7 @@ typedef enum {
   MWSHT_E_SYMMETRY = 4,     /* SymmetryError           (mw.py:543-547)            */
   MWSHT_E_VALUE = 5,        /* ValueError: unknown recursion (mw.py:562-566)      */
   MWSHT_E_CUDA = 6,         /* CUDA runtime failure                              */
-  MWSHT_E_CUFFT = 7,        /* cuFFT failure                                     */
+  MWSHT_E_DEGREE = 7,       /* UnsupportedDegreeError  (errors.py:24-25): L > 4096 */
   MWSHT_E_NOMEM = 8,        /* device or host allocation failure                 */
   MWSHT_E_PLAN = 9          /* null / mismatched plan                            */
 } mwsht_status;
@@ -62,12 +70,12 @@ typedef struct mwsht_plan mwsht_plan;
 /* Library / device introspection. */
 const char *mwsht_version(void);
 const char *mwsht_status_string(int status);
-/* Last CUDA / cuFFT error text recorded by this thread (for diagnostics). */
+/* Last CUDA error text recorded by this thread (for diagnostics). */
 const char *mwsht_last_error(void);
 
-/* Plan for band-limit L on `device` (cudaGetDevice() if < 0).  Owns the cuFFT
- * plans, the quadrature-weight spectrum (cf. the reference's _CONV_CACHE,
- * mw.py:225-241), the 1-D recursion tables, the l-independent top-row seed
+/* Plan for band-limit L on `device` (cudaGetDevice() if < 0).  Owns the FFT
+ * engine's tables (chirps, twiddles, the quadrature-weight spectrum: cf. the
+ * reference's _CONV_CACHE, mw.py:225-241), the 1-D recursion tables, the l-independent top-row seed
  * table sqrt(C(2n,n+k))/2^n, per-spin spin-column tables (built lazily), and
  * scratch buffers for up to `max_batch` maps.  Creation synchronises. */
 int mwsht_plan_create(int L, int device, int max_batch, mwsht_plan **out);
@@ -151,9 +159,9 @@ int mwsht_flm_core_real(mwsht_plan *plan, const void *gfold, int use_trapani, vo
 int mwsht_forward_stages_z(mwsht_plan *plan, const void *samples, void *gfold, int spin,
                            void *stream);
 
-/* Kernel launches issued by the most recent transform call on this plan
- * (own kernels only, cuFFT excluded / included). */
-int mwsht_plan_last_launches(const mwsht_plan *plan, int *own, int *cufft);
+/* Kernel launches issued by the most recent transform call on this plan (all
+ * of them are this library's own kernels: no library FFT/BLAS is called). */
+int mwsht_plan_last_launches(const mwsht_plan *plan, int *own);
 
 /* ------------------------------------------------ m-column / ring sharding ----
  * Stage entry points of ONE complex map split over ranks: a

@@ -8,7 +8,7 @@ import ctypes
 import os
 
 from .errors import (ContractViolationError, DeviceError, InvalidBandLimitError,
-                     InvalidSpinError, SymmetryError)
+                     InvalidSpinError, SymmetryError, UnsupportedDegreeError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmwsht.so")
@@ -24,7 +24,7 @@ _EXC = {
     4: SymmetryError,
     5: ValueError,
     6: DeviceError,
-    7: DeviceError,
+    7: UnsupportedDegreeError,
     8: MemoryError,
     9: DeviceError,
 }
@@ -53,7 +53,7 @@ _SIGS = {
     "mwsht_fmm_core_real": ([_P, _P, _P, _I, _P, _P], _I),
     "mwsht_flm_core_real": ([_P, _P, _I, _P, _P], _I),
     "mwsht_forward_stages_z": ([_P, _P, _P, _I, _P], _I),
-    "mwsht_plan_last_launches": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
+    "mwsht_plan_last_launches": ([_P, ctypes.POINTER(_I)], _I),
     "mwsht_plan_set_timing": ([_P, _I], _I),
     "mwsht_plan_set_paired": ([_P, _I], _I),
     "mwsht_shard_forward_phi": ([_P, _P, _I, _I, _P, _P], _I),

@@ -19,20 +19,11 @@
 namespace mwsht {
 void launch_inverse_core(const InvArgs& a, int ntiles, int nmaps, bool real, cudaStream_t st);
 void launch_forward_core(const FwdArgs& a, int ntiles, int nmaps, bool real, cudaStream_t st);
-void launch_extend_transpose(bool real, const double2* A, double2* B, int L, int N, int spin,
-                             double scale, long long as, long long bs, int nm, cudaStream_t st);
-void launch_pad_twist(const double2* B, double2* C, int rows, int L, int N, int P, long long bs,
-                      long long cs, int nm, cudaStream_t st);
-void launch_mul_spectrum(double2* C, const double2* W, int P, long long nrows, cudaStream_t st);
-void launch_fold(bool real, bool from_conv, const double2* src, double2* gfT, int L, int P,
-                 int ldw, int spin, long long ss, long long gs, int nm, cudaStream_t st);
+void launch_fold(bool real, const double2* gf, double2* gfT, int L, int ldw, cudaStream_t st);
 void launch_T2_to_fold(bool real, const double2* gfT, double2* gf, int L, int ldw, cudaStream_t st);
 void launch_inv_prescale(bool real, const double2* in, int in_mode, const double* cl,
                          const double* A, int L, int ldw, double2* gp, long long is, long long gs,
                          int nm, cudaStream_t st);
-void launch_transpose(const double2* in, double2* out, int rows, int cols, cudaStream_t st);
-void launch_untranspose(bool real, const double2* S, double2* Out, int L, int N, long long ss,
-                        long long os, int nm, cudaStream_t st);
 void launch_reality(const double2* f, int L, unsigned long long* red, unsigned long long* host,
                     cudaStream_t st);
 void fft_launch(int which, bool real, const fft::FftArgs& a, int nsm, cudaStream_t st);
@@ -99,6 +90,41 @@ struct mwsht_plan {
   double* colc = nullptr;  // [blk32(l, m)] = C_l(m)
   std::vector<long double> hl_A, hl_V, hl_Bt, hl_lam, hl_kap;  // host tables for the spin builds
   std::mutex mu;
+  // Stream hand-off of the plan's scratch (bufA/B/G, FFT scratch, reality
+  // slots): every call records `handoff` on its stream when it has enqueued
+  // its work, and a call on a different stream first waits on it, so callers
+  // on several streams/threads serialise on the device instead of racing on
+  // the scratch (reentrancy; cli.py:205-207 thread pool).
+  cudaEvent_t handoff = nullptr;
+  cudaStream_t last_st = nullptr;
+  bool has_last = false;
+  bool capturing = false;  // inside an internal graph capture: no hand-off
+};
+
+// Restores the caller's current device on return from every entry point.
+struct DevGuard {
+  int prev = -1;
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Orders this call after the previous user of the plan's scratch (see
+// mwsht_plan::handoff).  Caller holds p->mu.
+struct StreamUse {
+  mwsht_plan* p;
+  cudaStream_t st;
+  StreamUse(mwsht_plan* p_, cudaStream_t s) : p(p_), st(s) {
+    if (p->handoff && !p->capturing && p->has_last && p->last_st != st)
+      cudaStreamWaitEvent(st, p->handoff, 0);
+  }
+  ~StreamUse() {
+    if (p->handoff && !p->capturing) {
+      cudaEventRecord(p->handoff, st);
+      p->last_st = st;
+      p->has_last = true;
+    }
+  }
 };
 
 static int dev_alloc(mwsht_plan* p, void** ptr, size_t bytes) {
@@ -499,7 +525,9 @@ static int build_fft_tables(mwsht_plan* p) {
   p->H = M / 2;
   p->logH = 0;
   while ((1 << p->logH) < p->H) p->logH++;
-  if (p->H > 8192) return fail(MWSHT_E_BAND_LIMIT, "plan_create", "fused FFT engine supports L <= 4096");
+  if (p->H > 8192)
+    return fail(MWSHT_E_DEGREE, "plan_create",
+                "band limit above the documented cap L <= 4096 (one FFT half-convolution per SM)");
   const ld PI = 3.141592653589793238462643383279502884L;
   std::vector<double2> tw(M / 4 + 1), ch(N), rho(N), kf(M, make_double2(0, 0)), ki(kf), kw(kf);
   std::vector<double2> cen(N), wnk(N), rho2(N);
@@ -573,9 +601,14 @@ static int build_fft_tables(mwsht_plan* p) {
   return MWSHT_OK;
 }
 
-static int check_plan(mwsht_plan* p) {
+static int check_plan(mwsht_plan* p, DevGuard& g) {
   if (!p) return fail(MWSHT_E_PLAN, "plan", "null plan");
-  CU(cudaSetDevice(p->device));
+  int cur = -1;
+  CU(cudaGetDevice(&cur));
+  if (cur != p->device) {
+    CU(cudaSetDevice(p->device));
+    g.prev = cur;
+  }
   return MWSHT_OK;
 }
 
@@ -665,13 +698,15 @@ static int forward_stages(mwsht_plan* p, int nm, const void* samples, bool real,
 
 static int do_forward(mwsht_plan* p, int nm, const void* samples, void* flm, int spin, bool real,
                       int recursion, void* stream) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p))) return rc;
+  if ((rc = check_plan(p, dg))) return rc;
   if ((rc = check_rec(recursion))) return rc;
   if ((rc = check_spin(p, spin))) return rc;
   if (real && spin != 0) return fail(MWSHT_E_SPIN, "forward_real", "spin 0 only");
   if (nm < 1 || nm > p->max_batch) return fail(MWSHT_E_CONTRACT, "nmaps", "exceeds plan max_batch");
   std::lock_guard<std::mutex> lk(p->mu);
+  StreamUse su(p, (cudaStream_t)stream);
   if ((rc = build_spin(p, spin))) return rc;
   p->own_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
@@ -691,13 +726,15 @@ static int do_forward(mwsht_plan* p, int nm, const void* samples, void* flm, int
 
 static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int spin, bool real,
                       int recursion, void* stream) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p))) return rc;
+  if ((rc = check_plan(p, dg))) return rc;
   if ((rc = check_rec(recursion))) return rc;
   if ((rc = check_spin(p, spin))) return rc;
   if (real && spin != 0) return fail(MWSHT_E_SPIN, "inverse_real", "spin 0 only");
   if (nm < 1 || nm > p->max_batch) return fail(MWSHT_E_CONTRACT, "nmaps", "exceeds plan max_batch");
   std::lock_guard<std::mutex> lk(p->mu);
+  StreamUse su(p, (cudaStream_t)stream);
   if ((rc = build_spin(p, spin))) return rc;
   p->own_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
@@ -753,7 +790,7 @@ const char* mwsht_status_string(int s) {
     case MWSHT_E_SYMMETRY: return "symmetry violation";
     case MWSHT_E_VALUE: return "invalid value";
     case MWSHT_E_CUDA: return "CUDA error";
-    case MWSHT_E_CUFFT: return "cuFFT error";
+    case MWSHT_E_DEGREE: return "unsupported degree";
     case MWSHT_E_NOMEM: return "out of memory";
     case MWSHT_E_PLAN: return "invalid plan";
   }
@@ -768,6 +805,11 @@ int mwsht_plan_create(int L, int device, int max_batch, mwsht_plan** out) {
   if (L < 1) return fail(MWSHT_E_BAND_LIMIT, "plan_create", "band limit must be >= 1");
   if (max_batch < 1) max_batch = 1;
   if (LDBL_MANT_DIG < 64) return fail(MWSHT_E_VALUE, "plan_create", "needs 80-bit long double");
+  DevGuard dg;
+  {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess) dg.prev = cur;
+  }
   mwsht_plan* p = new mwsht_plan();
   int rc;
   if (device < 0) {
@@ -800,6 +842,11 @@ int mwsht_plan_create(int L, int device, int max_batch, mwsht_plan** out) {
     mwsht_plan_destroy(p);
     return rc;
   }
+  e = cudaEventCreateWithFlags(&p->handoff, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    mwsht_plan_destroy(p);
+    return fail(MWSHT_E_CUDA, "cudaEventCreate", cudaGetErrorString(e));
+  }
   e = cudaHostAlloc((void**)&p->red_host, 2 * sizeof(unsigned long long), cudaHostAllocMapped);
   if (e == cudaSuccess)
     e = cudaHostGetDevicePointer((void**)&p->red_host_dev, p->red_host, 0);
@@ -820,8 +867,14 @@ int mwsht_plan_create(int L, int device, int max_batch, mwsht_plan** out) {
 
 int mwsht_plan_destroy(mwsht_plan* p) {
   if (!p) return MWSHT_OK;
+  DevGuard dg;
+  {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != p->device) dg.prev = cur;
+  }
   cudaSetDevice(p->device);
   cudaDeviceSynchronize();
+  if (p->handoff) cudaEventDestroy(p->handoff);
   for (auto& d : p->ev)
     for (auto& e : d)
       if (e) cudaEventDestroy(e);
@@ -834,8 +887,9 @@ int mwsht_plan_destroy(mwsht_plan* p) {
 size_t mwsht_plan_device_bytes(const mwsht_plan* p) { return p ? p->bytes : 0; }
 
 int mwsht_plan_prepare_spin(mwsht_plan* p, int spin) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p)) || (rc = check_spin(p, spin))) return rc;
+  if ((rc = check_plan(p, dg)) || (rc = check_spin(p, spin))) return rc;
   std::lock_guard<std::mutex> lk(p->mu);
   return build_spin(p, spin);
 }
@@ -872,9 +926,11 @@ int mwsht_inverse_z_batch(mwsht_plan* p, int nmaps, const void* flm, void* sampl
 
 int mwsht_reality_residual(mwsht_plan* p, const void* flm, double* worst_host, double* tol_host,
                            void* stream) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p))) return rc;
+  if ((rc = check_plan(p, dg))) return rc;
   std::lock_guard<std::mutex> lk(p->mu);
+  StreamUse su(p, (cudaStream_t)stream);
   cudaStream_t st = (cudaStream_t)stream;
   launch_reality((const double2*)flm, p->L, p->red, p->red_host_dev, st);
   LAUNCHED(p);
@@ -892,8 +948,9 @@ int mwsht_reality_residual(mwsht_plan* p, const void* flm, double* worst_host, d
 
 int mwsht_reality_residual_async(mwsht_plan* p, const void* flm, unsigned long long* dev_worst_peak,
                                  void* stream) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p))) return rc;
+  if ((rc = check_plan(p, dg))) return rc;
   if (!dev_worst_peak) return fail(MWSHT_E_CONTRACT, "reality_residual_async", "null result buffer");
   launch_reality((const double2*)flm, p->L, dev_worst_peak, nullptr, (cudaStream_t)stream);
   CU(cudaGetLastError());
@@ -902,10 +959,12 @@ int mwsht_reality_residual_async(mwsht_plan* p, const void* flm, unsigned long l
 
 int mwsht_fmm_core(mwsht_plan* p, const void* flm2d, const double* cl, int spin, int use_trapani,
                    void* T, void* stream) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p)) || (rc = check_spin(p, spin))) return rc;
+  if ((rc = check_plan(p, dg)) || (rc = check_spin(p, spin))) return rc;
   (void)use_trapani;
   std::lock_guard<std::mutex> lk(p->mu);
+  StreamUse su(p, (cudaStream_t)stream);
   if ((rc = build_spin(p, spin))) return rc;
   p->own_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
@@ -922,10 +981,12 @@ int mwsht_fmm_core(mwsht_plan* p, const void* flm2d, const double* cl, int spin,
 
 int mwsht_fmm_core_real(mwsht_plan* p, const void* flm_half, const double* cl, int use_trapani,
                         void* T, void* stream) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p))) return rc;
+  if ((rc = check_plan(p, dg))) return rc;
   (void)use_trapani;
   std::lock_guard<std::mutex> lk(p->mu);
+  StreamUse su(p, (cudaStream_t)stream);
   p->own_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
   launch_inv_prescale(true, (const double2*)flm_half, 1, cl, p->tabs.A, p->L, p->ldw, p->bufG, 0,
@@ -941,15 +1002,16 @@ int mwsht_fmm_core_real(mwsht_plan* p, const void* flm_half, const double* cl, i
 
 int mwsht_flm_core(mwsht_plan* p, const void* gfold, int spin, int use_trapani, void* R,
                    void* stream) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p)) || (rc = check_spin(p, spin))) return rc;
+  if ((rc = check_plan(p, dg)) || (rc = check_spin(p, spin))) return rc;
   (void)use_trapani;
   std::lock_guard<std::mutex> lk(p->mu);
+  StreamUse su(p, (cudaStream_t)stream);
   if ((rc = build_spin(p, spin))) return rc;
   p->own_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
-  launch_fold(false, false, (const double2*)gfold, p->bufG, p->L, 0, p->ldw, spin, 0,
-              p->strideG, 1, st);
+  launch_fold(false, (const double2*)gfold, p->bufG, p->L, p->ldw, st);
   LAUNCHED(p);
   FwdArgs a = fwd_args(p, spin);
   a.out = (double2*)R;
@@ -962,14 +1024,15 @@ int mwsht_flm_core(mwsht_plan* p, const void* gfold, int spin, int use_trapani, 
 }
 
 int mwsht_flm_core_real(mwsht_plan* p, const void* gfold, int use_trapani, void* R, void* stream) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p))) return rc;
+  if ((rc = check_plan(p, dg))) return rc;
   (void)use_trapani;
   std::lock_guard<std::mutex> lk(p->mu);
+  StreamUse su(p, (cudaStream_t)stream);
   p->own_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
-  launch_fold(true, false, (const double2*)gfold, p->bufG, p->L, 0, p->ldw, 0, 0, p->strideG,
-              1, st);
+  launch_fold(true, (const double2*)gfold, p->bufG, p->L, p->ldw, st);
   LAUNCHED(p);
   FwdArgs a = fwd_args(p, 0);
   a.out = (double2*)R;
@@ -982,9 +1045,11 @@ int mwsht_flm_core_real(mwsht_plan* p, const void* gfold, int use_trapani, void*
 
 int mwsht_forward_stages_z(mwsht_plan* p, const void* samples, void* gfold, int spin,
                            void* stream) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p)) || (rc = check_spin(p, spin))) return rc;
+  if ((rc = check_plan(p, dg)) || (rc = check_spin(p, spin))) return rc;
   std::lock_guard<std::mutex> lk(p->mu);
+  StreamUse su(p, (cudaStream_t)stream);
   p->own_launches = 0;
   if ((rc = forward_stages(p, 1, samples, false, spin, (cudaStream_t)stream))) return rc;
   launch_T2_to_fold(false, p->bufG, (double2*)gfold, p->L, p->ldw, (cudaStream_t)stream);
@@ -1000,10 +1065,12 @@ static int check_range(mwsht_plan* p, int m0, int m1) {
 
 int mwsht_shard_forward_phi(mwsht_plan* p, const void* samples_rows, int t0, int t1, void* AT,
                             void* stream) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p))) return rc;
+  if ((rc = check_plan(p, dg))) return rc;
   if (t0 < 0 || t1 > p->L || t0 >= t1) return fail(MWSHT_E_CONTRACT, "shard", "bad ring range");
   std::lock_guard<std::mutex> lk(p->mu);
+  StreamUse su(p, (cudaStream_t)stream);
   p->own_launches = 0;
   fft::FftArgs a = fft_args(p);
   a.nrows = t1 - t0;
@@ -1019,9 +1086,11 @@ int mwsht_shard_forward_phi(mwsht_plan* p, const void* samples_rows, int t0, int
 
 int mwsht_shard_forward_rest(mwsht_plan* p, const void* AT, int m0, int m1, int spin, void* flm,
                              void* stream) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p)) || (rc = check_spin(p, spin)) || (rc = check_range(p, m0, m1))) return rc;
+  if ((rc = check_plan(p, dg)) || (rc = check_spin(p, spin)) || (rc = check_range(p, m0, m1))) return rc;
   std::lock_guard<std::mutex> lk(p->mu);
+  StreamUse su(p, (cudaStream_t)stream);
   if ((rc = build_spin(p, spin))) return rc;
   mwsht_plan::TileSet* ts;
   if ((rc = range_tiles(p, m0, m1, &ts))) return rc;
@@ -1052,9 +1121,11 @@ int mwsht_shard_forward_rest(mwsht_plan* p, const void* AT, int m0, int m1, int 
 
 int mwsht_shard_inverse_front(mwsht_plan* p, const void* flm, int m0, int m1, int spin, void* OUT,
                               void* stream) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p)) || (rc = check_spin(p, spin)) || (rc = check_range(p, m0, m1))) return rc;
+  if ((rc = check_plan(p, dg)) || (rc = check_spin(p, spin)) || (rc = check_range(p, m0, m1))) return rc;
   std::lock_guard<std::mutex> lk(p->mu);
+  StreamUse su(p, (cudaStream_t)stream);
   if ((rc = build_spin(p, spin))) return rc;
   mwsht_plan::TileSet* ts;
   if ((rc = range_tiles(p, m0, m1, &ts))) return rc;
@@ -1090,10 +1161,12 @@ int mwsht_shard_inverse_front(mwsht_plan* p, const void* flm, int m0, int m1, in
 
 int mwsht_shard_inverse_phi(mwsht_plan* p, const void* OUT, int t0, int t1, void* samples_rows,
                             void* stream) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p))) return rc;
+  if ((rc = check_plan(p, dg))) return rc;
   if (t0 < 0 || t1 > p->L || t0 >= t1) return fail(MWSHT_E_CONTRACT, "shard", "bad ring range");
   std::lock_guard<std::mutex> lk(p->mu);
+  StreamUse su(p, (cudaStream_t)stream);
   p->own_launches = 0;
   fft::FftArgs f = fft_args(p);
   f.nrows = t1 - t0;
@@ -1108,8 +1181,9 @@ int mwsht_shard_inverse_phi(mwsht_plan* p, const void* OUT, int t0, int t1, void
 }
 
 int mwsht_plan_set_paired(mwsht_plan* p, int mode) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p))) return rc;
+  if ((rc = check_plan(p, dg))) return rc;
   if (mode < -1 || mode > 1) return fail(MWSHT_E_VALUE, "paired", "mode must be -1, 0 or 1");
   std::lock_guard<std::mutex> lk(p->mu);
   p->paired_mode = mode;
@@ -1117,8 +1191,9 @@ int mwsht_plan_set_paired(mwsht_plan* p, int mode) {
 }
 
 int mwsht_plan_set_timing(mwsht_plan* p, int on) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p))) return rc;
+  if ((rc = check_plan(p, dg))) return rc;
   for (auto& d : p->ev)
     for (auto& e : d)
       if (!e) CU(cudaEventCreate(&e));
@@ -1127,8 +1202,9 @@ int mwsht_plan_set_timing(mwsht_plan* p, int on) {
 }
 
 int mwsht_plan_last_timing(mwsht_plan* p, int inverse, float* core_ms, float* stages_ms) {
+  DevGuard dg;
   int rc;
-  if ((rc = check_plan(p))) return rc;
+  if ((rc = check_plan(p, dg))) return rc;
   if (!p->timing) return fail(MWSHT_E_VALUE, "last_timing", "timing not enabled");
   cudaEvent_t* e = p->ev[inverse ? 1 : 0];
   CU(cudaEventSynchronize(e[2]));
@@ -1140,10 +1216,9 @@ int mwsht_plan_last_timing(mwsht_plan* p, int inverse, float* core_ms, float* st
   return MWSHT_OK;
 }
 
-int mwsht_plan_last_launches(const mwsht_plan* p, int* own, int* cufft) {
+int mwsht_plan_last_launches(const mwsht_plan* p, int* own) {
   if (!p) return MWSHT_E_PLAN;
   if (own) *own = p->own_launches;
-  if (cufft) *cufft = 0;  // no library FFT launches: the FFT stages are fused kernels
   return MWSHT_OK;
 }
 

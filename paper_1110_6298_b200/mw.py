@@ -5,8 +5,15 @@ Mirrors the reference's public path (pkg/src/torusht/mw.py): the containers
 ``forward`` (:365), ``inverse`` (:419), ``forward_real`` (:469) and
 ``inverse_real`` (:524), with the same arguments, flat coefficient layout
 l(l+1)+m, MW grid (L rings x 2L-1 azimuths), validation order and exception
-types.  All arithmetic runs in libmwsht.so (hand-written sm_100a kernels +
-cuFFT) through the C ABI in include/mwsht.h; there is no CPU fallback.
+types.  All arithmetic runs in libmwsht.so (hand-written sm_100a kernels,
+including the FFT stages; no cuFFT/cuBLAS) through the C ABI in
+include/mwsht.h; there is no CPU fallback.
+
+Band limits: every L >= 1 up to L = 4096 (the FFT engine's documented cap);
+larger L raises UnsupportedDegreeError (errors.py:24-25) when the plan is
+built.  Calls are reentrant: plans are shared per (L, device), and the
+library orders calls from different threads/streams on the device so they
+never share scratch in flight (include/mwsht.h).
 
 Arrays may be numpy arrays (drop-in: results come back as numpy, host<->device
 copies included) or torch tensors (results stay on the tensor's CUDA device;
@@ -137,7 +144,7 @@ def mw_grid_phis(L):
 # ------------------------------------------------------------------ plans
 
 class Plan:
-    """Owns one native plan (cuFFT plans, tables, scratch) for (L, device, batch)."""
+    """Owns one native plan (FFT tables, recursion tables, scratch) for (L, device, batch)."""
 
     def __init__(self, L, device, max_batch=1):
         lib = _lib.load()
@@ -154,10 +161,10 @@ class Plan:
         return int(_lib.load().mwsht_plan_device_bytes(self.handle))
 
     def last_launches(self):
-        own, cf = _lib.ctypes.c_int(), _lib.ctypes.c_int()
-        _lib.load().mwsht_plan_last_launches(self.handle, _lib.ctypes.byref(own),
-                                             _lib.ctypes.byref(cf))
-        return own.value, cf.value
+        """Kernel launches of the most recent call on this plan (all our own)."""
+        own = _lib.ctypes.c_int()
+        _lib.load().mwsht_plan_last_launches(self.handle, _lib.ctypes.byref(own))
+        return own.value
 
     def set_paired(self, mode):
         """Inverse-core tiling for spin 0: -1 (default) paired tiles for single
@@ -173,25 +180,39 @@ class Plan:
             _lib.load().mwsht_plan_destroy(self.handle)
             self.handle = None
 
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
+
 
 _PLANS = {}
 _PLANS_LOCK = threading.Lock()
 
 
 def get_plan(L, device=None, max_batch=1):
-    """Cached plan for band-limit L on a CUDA device (cf. _CONV_CACHE, mw.py:225)."""
+    """Cached plan for band-limit L on a CUDA device (cf. _CONV_CACHE, mw.py:225).
+
+    One plan per (L, device): batch capacity is rounded up to a power of two,
+    and a request beyond the cached capacity replaces the cached plan (the old
+    one is freed once no caller holds it), so growing batches never keep
+    several plans' scratch alive."""
     if device is None:
         device = torch.cuda.current_device()
     device = int(device)
+    cap = 1
+    while cap < max_batch:
+        cap *= 2
     with _PLANS_LOCK:
-        best = None
-        for (l_, d_, b_), p in _PLANS.items():
-            if l_ == L and d_ == device and b_ >= max_batch and (best is None or b_ < best.max_batch):
-                best = p
-        if best is None:
-            best = Plan(L, device, max_batch)
-            _PLANS[(L, device, max_batch)] = best
-        return best
+        p = _PLANS.get((L, device))
+        if p is None or p.max_batch < cap:
+            if p is not None:
+                del _PLANS[(L, device)]
+                p = None  # freed when the last in-flight caller drops it
+            p = Plan(L, device, cap)
+            _PLANS[(L, device)] = p
+        return p
 
 
 def clear_plans():

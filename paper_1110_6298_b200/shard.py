@@ -46,6 +46,9 @@ def balanced_m_splits(L, parts, align=32):
     rounded to multiples of `align` (the core's tile width)."""
     if parts <= 1:
         return [0, L]
+    if L < align * parts:
+        raise ValueError(f"cannot split L={L} into {parts} order ranges of width >= {align} "
+                         f"(needs L >= {align * parts})")
     w = np.cumsum(column_work(L))
     total = w[-1]
     bounds = [0]
@@ -53,7 +56,10 @@ def balanced_m_splits(L, parts, align=32):
         target = total * k / parts
         b = int(np.searchsorted(w, target)) + 1
         b = int(round(b / align)) * align
-        b = min(max(b, bounds[-1] + align), L - align * (parts - k))
+        # the last ranges each need >= align columns; interior bounds stay on the
+        # align grid (the shard entry points require it, plan.cu check_range)
+        hi = (L - align * (parts - k)) // align * align
+        b = min(max(b, bounds[-1] + align), hi)
         bounds.append(b)
     bounds.append(L)
     if any(b1 <= b0 for b0, b1 in zip(bounds, bounds[1:])):

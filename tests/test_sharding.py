@@ -116,3 +116,14 @@ def _maps(rank, world):
 
 def test_map_sharding_gather_gloo():
     assert max(_run(_maps).values()) == 0.0
+
+
+def test_balanced_splits_stay_on_tile_grid_or_refuse():
+    # every interior bound must be a multiple of the tile width (the shard entry
+    # points reject anything else); too small L for the rank count is refused
+    for L, parts in [(250, 7), (256, 8), (300, 4), (97, 3), (4096, 8), (1000, 5)]:
+        b = shard.balanced_m_splits(L, parts)
+        assert all(x % 32 == 0 for x in b[1:-1]), (L, parts, b)
+        assert all(y - x >= 32 for x, y in zip(b, b[1:]))
+    with pytest.raises(ValueError):
+        shard.balanced_m_splits(250, 8)
