@@ -167,24 +167,44 @@ int mwsht_plan_last_launches(const mwsht_plan *plan, int *own);
  * Stage entry points of ONE complex map split over ranks: a
  * rank owns the orders m0 <= |m| < m1 (m0, m1 multiples of 32, or m1 = L) and
  * the rings t0 <= t < t1.  With the l-recursion / Trapani-column cores every
- * chain is independent, so no Delta halo is exchanged; the only exchange is
- * one all-to-all transpose of the ring spectra per transform, done by the
- * caller on its own buffers (paper_1110_6298_b200/shard.py, NCCL):
- *   forward: shard_forward_phi (rings t0..t1 of `samples_rows` -> columns
- *            t0..t1 of AT (N x L, row bin(m))) ; all-to-all so that AT holds
- *            rows bin(+-m), m0 <= |m| < m1, for all t ; shard_forward_rest
- *            (theta stage + forward core) writes flm[l(l+1)+m] for those m.
- *   inverse: shard_inverse_front (core + theta synthesis) writes columns
- *            bin(+-m) of OUT (L x N) ; all-to-all so that OUT holds rows
- *            t0..t1 ; shard_inverse_phi writes those rings of the samples. */
-int mwsht_shard_forward_phi(mwsht_plan *plan, const void *samples_rows, int t0, int t1, void *AT,
-                            void *stream);
-int mwsht_shard_forward_rest(mwsht_plan *plan, const void *AT, int m0, int m1, int spin, void *flm,
-                             void *stream);
+ * chain is independent, so no Delta halo is exchanged; the only
+ * exchange is one all-to-all transpose of the ring spectra per transform,
+ * plus an all-gather of the forward's coefficient blocks, done by the caller
+ * (paper_1110_6298_b200/shard.py, NCCL) on buffers these kernels read and
+ * write in place:
+ *   forward: shard_forward_phi writes the phi spectra of rings t0..t1 straight
+ *            into the all-to-all SEND layout (bin k, ring t at
+ *            out[row_off[k] + t - t0]); after the all-to-all,
+ *            shard_forward_rest reads the RECEIVE layout (local order row i,
+ *            ring t at in[col_off[t] + i * col_stride[t]]), runs the theta
+ *            stage and the forward core for its orders and writes either the
+ *            flat flm (packed = 0, its orders only) or its packed coefficient
+ *            block (packed = 1: l-major, orders -hi..-max(m0,1), m0..hi per
+ *            degree); after an all-gather of the blocks shard_unpack_flm
+ *            rebuilds the flat flm on every rank.
+ *   inverse: shard_inverse_front (prescale + core + theta synthesis of its
+ *            orders) writes ring t of local order row i to out[row_off[t] + i]
+ *            (the SEND layout); after the all-to-all, shard_inverse_phi reads
+ *            ring t, bin n at in[col_off[n] + (t - t0) * col_stride[n]] and
+ *            writes its rings of the samples.
+ * Local order row i enumerates +m0..+(m1-1), then -m0..-(m1-1) (m = 0 once).
+ * The offset tables are device arrays built by the caller (shard.py); passing
+ * NULL tables selects the dense single-GPU layouts (AT: N x L, row bin(m);
+ * OUT: L x N, column bin(m)), which emulate_mcolumn uses. */
+int mwsht_shard_forward_phi(mwsht_plan *plan, const void *samples_rows, int t0, int t1,
+                            const long long *row_off, void *out, void *stream);
+int mwsht_shard_forward_rest(mwsht_plan *plan, const void *in, int m0, int m1,
+                             const long long *col_off, const int *col_stride, int spin, void *flm,
+                             int packed, void *stream);
 int mwsht_shard_inverse_front(mwsht_plan *plan, const void *flm, int m0, int m1, int spin,
-                              void *OUT, void *stream);
-int mwsht_shard_inverse_phi(mwsht_plan *plan, const void *OUT, int t0, int t1, void *samples_rows,
+                              const long long *row_off, void *out, void *stream);
+int mwsht_shard_inverse_phi(mwsht_plan *plan, const void *in, int t0, int t1,
+                            const long long *col_off, const int *col_stride, void *samples_rows,
                             void *stream);
+/* gathered: world blocks of maxlen complex values (rank r's packed block at
+ * r * maxlen); bounds: device int[world + 1] order boundaries. */
+int mwsht_shard_unpack_flm(mwsht_plan *plan, const void *gathered, long long maxlen,
+                           const int *bounds, int world, void *flm, void *stream);
 
 /* Inverse-core tiling (no reference counterpart; a scheduling choice only).
  * Paired tiles: each (m', m) chain with m' > m also produces the transposed

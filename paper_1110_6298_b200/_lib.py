@@ -56,10 +56,11 @@ _SIGS = {
     "mwsht_plan_last_launches": ([_P, ctypes.POINTER(_I)], _I),
     "mwsht_plan_set_timing": ([_P, _I], _I),
     "mwsht_plan_set_paired": ([_P, _I], _I),
-    "mwsht_shard_forward_phi": ([_P, _P, _I, _I, _P, _P], _I),
-    "mwsht_shard_forward_rest": ([_P, _P, _I, _I, _I, _P, _P], _I),
-    "mwsht_shard_inverse_front": ([_P, _P, _I, _I, _I, _P, _P], _I),
-    "mwsht_shard_inverse_phi": ([_P, _P, _I, _I, _P, _P], _I),
+    "mwsht_shard_forward_phi": ([_P, _P, _I, _I, _P, _P, _P], _I),
+    "mwsht_shard_forward_rest": ([_P, _P, _I, _I, _P, _P, _I, _P, _I, _P], _I),
+    "mwsht_shard_inverse_front": ([_P, _P, _I, _I, _I, _P, _P, _P], _I),
+    "mwsht_shard_inverse_phi": ([_P, _P, _I, _I, _P, _P, _P, _P], _I),
+    "mwsht_shard_unpack_flm": ([_P, _P, ctypes.c_longlong, _P, _I, _P, _P], _I),
     "mwsht_plan_last_timing": ([_P, _I, ctypes.POINTER(ctypes.c_float),
                                 ctypes.POINTER(ctypes.c_float)], _I),
     "mwsht_fp64_probe": ([_I, ctypes.POINTER(ctypes.c_double),

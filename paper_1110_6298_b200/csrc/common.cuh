@@ -145,7 +145,24 @@ struct FwdArgs {
   int ldw;
   int nmaps;  // maps in the batch (set by launch_forward_core)
   long long in_stride, out_stride;
+  int m0, m1;  // out_mode 2: the shard's order range (packed flm, shard_flm_index)
 };
+
+// Packed coefficient block of an order-range shard m0 <= |m| < m1 (m-column
+// sharding, out_mode 2 of the forward core): l-major, and within a degree
+// the orders in increasing m (-hi .. -max(m0,1), then m0 .. hi, hi =
+// min(l, m1-1)), i.e. the flat l(l+1)+m layout restricted to the shard.
+__host__ __device__ __forceinline__ long long shard_flm_base(int l, int m0, int m1) {
+  const long long k = l - m0 < 0 ? 0 : (l - m0 > m1 - m0 ? m1 - m0 : l - m0);
+  const long long s1 = k * (k + 1) / 2 + (long long)(m1 - m0) * (l > m1 ? l - m1 : 0);
+  return 2 * s1 - (m0 == 0 ? l : 0);
+}
+__host__ __device__ __forceinline__ long long shard_flm_index(int l, int m, int m0, int m1) {
+  const int hi = l < m1 - 1 ? l : m1 - 1;
+  const int mn = m0 > 0 ? m0 : 1;
+  const long long b = shard_flm_base(l, m0, m1);
+  return m < 0 ? b + (m + hi) : b + (hi - mn + 1) + (m - m0);
+}
 
 namespace fft {
 // Arguments of the fused FFT-stage kernels (fft.cu).
@@ -167,6 +184,16 @@ struct FftArgs {
   int nrows, nmaps;
   int m0, m1;  // theta kernels: rows are the orders m with m0 <= |m| < m1 (full: 0, L)
   int t0;      // phi kernels: rows are the rings t0 .. t0+nrows-1
+  // m-column sharding exchange layouts (shard.py builds the tables; nullptr =
+  // dense layouts).  Local row i of an order-range shard is row_order(i).
+  //   k_phi_fwd   out: bin k, ring t   -> out[row_off[k] + (t - t0)]
+  //   k_theta_fwd in:  row i, ring t   -> in[col_off[t] + i * col_stride[t]]
+  //   k_theta_inv out: row i, ring t   -> out[row_off[t] + i]
+  //   k_phi_inv   in:  ring t, bin n   -> in[col_off[n] + (t - t0) * col_stride[n]]
+  const long long* row_off;
+  const long long* col_off;
+  const int* col_stride;
+  int spread;  // set by the launcher: rows dealt team-major (fft_impl.cuh first_row)
 };
 }  // namespace fft
 

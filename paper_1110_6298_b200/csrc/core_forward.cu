@@ -358,6 +358,16 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
       if (m > l) continue;
       const int e = i * NJ + j;
       const double2 Rp = make_double2(acc[mb][e][0], acc[mb][e][1]);
+      if (a.out_mode == 2) {  // shard's packed block (m-column sharding, common.cuh)
+        const double2 f = cscale(cmul(Rp, ipow(m + a.spin)), sgs * clv);
+        out[shard_flm_index(l, m, a.m0, a.m1)] = f;
+        if (m > 0) {
+          const double sl = (l & 1) ? -1.0 : 1.0;
+          const double2 Rn = make_double2(sl * acc[mb][e][2], sl * acc[mb][e][3]);
+          out[shard_flm_index(l, -m, a.m0, a.m1)] = cscale(cmul(Rn, ipow(a.spin - m)), sgs * clv);
+        }
+        continue;
+      }
       if (a.out_mode == 1) {
         if (REAL) {
           out[(long long)l * L + m] = Rp;

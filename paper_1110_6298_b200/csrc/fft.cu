@@ -1,786 +1,33 @@
-// Fused FFT stages (replaces cuFFT on the hot path): Bluestein DFTs of the odd
-// lengths N = 2L-1 (8191 is prime) and the quadrature-weight correlation, each
-// as an M-point FFT-convolution (M = P = 2^ceil(log2(4L-3))) run in one CTA's
-// shared memory.
-//
-// Engine.  A size-M FFT-convolution y = IDFT_M(DFT_M(x) . S) is split by its
-// first radix-2 step into two independent H = M/2 halves:
-//   half 0: x0[j] = x[j] + x[j+H],      half 1: x1[j] = (x[j] - x[j+H]) w_M^j
-//   z_h = DIT_H( DIF_H(x_h) . S_h )     (S_h = even / odd-index DFT_M(kernel))
-//   y[k] = z0[k] + w_M^-k z1[k],  y[k+H] = z0[k] - w_M^-k z1[k]   (unnormalised)
-// DIF_H leaves its output in digit-reversed order, the precomputed spectra S_h
-// are produced by the same DIF code (same order), and DIT_H consumes that
-// order, so no reordering pass exists anywhere.  H complex doubles (128 KB at
-// L = 4096) live in padded shared memory next to a quarter twiddle table;
-// z1 and intermediate rows spill to a per-CTA L2-resident scratch.
-//
-// Kernels (persistent: one CTA per SM loops over rows, rows x maps):
-//   k_phi_fwd    mw.py:149-158 / :489   samples row t -> AT[k][t] = 2pi/N DFT_N (transposed)
-//   k_theta_fwd  mw.py:161-285           AT row -> extension -> DFT_N -> twist -> weight
-//                                        correlation -> m' fold -> core staging (gfT)
-//   k_theta_inv  mw.py:441-446           spectrum row m -> IDFT_N -> Out[t][bin(m)], t < L
-//   k_phi_inv    mw.py:437-438 / :558    Out row t -> IDFT_N -> samples row t
-//   k_spectrum   plan time: S_0, S_1 of a length-M kernel
+// Dispatch of the fused FFT stages (fft_impl.cuh) over the compile-time
+// sizes H = 2^LOGH; each size is its own translation unit (fft_<LOGH>.cu) so
+// the instantiations build in parallel.
 #include "common.cuh"
-
-namespace mwsht {
-namespace fft {
-
-#ifndef MWSHT_FFT_THREADS
-#define MWSHT_FFT_THREADS 512  // 256 measured 5-35% slower (fewer warps per SM)
-#endif
-constexpr int kT = MWSHT_FFT_THREADS;  // threads per CTA
-
-
-
-// i-th order row of an |m| range [m0, m1): +m0..+(m1-1), then -m0..-(m1-1) (m = 0 once)
-__device__ __forceinline__ int row_order(int i, int m0, int m1, bool real) {
-  const int n = m1 - m0;
-  if (real || i < n) return m0 + i;
-  return -(m0 + (i - n) + (m0 == 0 ? 1 : 0));
-}
-
-// XOR swizzle of 16-byte elements inside each 128-byte segment: strided and
-// contiguous radix-R accesses of a warp land on distinct bank groups.
-__device__ __forceinline__ int phys(int i) { return i ^ ((i >> 3) & 7); }
-
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-// a * conj(b)
-__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
-  return make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
-}
-__device__ __forceinline__ double2 conjd(double2 a) { return make_double2(a.x, -a.y); }
-
-// w_M^e from the quarter table (M a power of two >= 8)
-__device__ __forceinline__ double2 omega(const double2* tw, int e, int M) {
-  e &= (M - 1);
-  const int q = M >> 2;
-  const int quad = e / q, r = e - quad * q;
-  const double2 v = tw[r];
-  switch (quad) {
-    case 0: return v;
-    case 1: return make_double2(v.y, -v.x);   // -i v
-    case 2: return make_double2(-v.x, -v.y);  // -v
-    default: return make_double2(-v.y, v.x);  // +i v
-  }
-}
-
-// x * e^{-2 pi i e/16} (CONJ: e^{+}), e a compile-time constant after unrolling:
-// multiples of pi/2 are sign/swap moves, odd multiples of pi/4 cost 2 adds + 2 muls.
-template <bool CONJ>
-__device__ __forceinline__ double2 rot16(double2 x, int e) {
-  constexpr double C1 = 0.92387953251128674, S1 = 0.38268343236508978, H = 0.70710678118654752;
-  e &= 15;
-  if (CONJ) e = (16 - e) & 15;
-  switch (e) {
-    case 0: return x;
-    case 4: return make_double2(x.y, -x.x);
-    case 8: return make_double2(-x.x, -x.y);
-    case 12: return make_double2(-x.y, x.x);
-    case 2: return make_double2(H * (x.x + x.y), H * (x.y - x.x));
-    case 6: return make_double2(H * (x.y - x.x), -H * (x.x + x.y));
-    case 10: return make_double2(-H * (x.x + x.y), H * (x.x - x.y));
-    case 14: return make_double2(H * (x.x - x.y), H * (x.x + x.y));
-    case 1: return cmul(x, make_double2(C1, -S1));
-    case 3: return cmul(x, make_double2(S1, -C1));
-    case 5: return cmul(x, make_double2(-S1, -C1));
-    case 7: return cmul(x, make_double2(-C1, -S1));
-    case 9: return cmul(x, make_double2(-C1, S1));
-    case 11: return cmul(x, make_double2(-S1, C1));
-    case 13: return cmul(x, make_double2(S1, C1));
-    default: return cmul(x, make_double2(C1, S1));
-  }
-}
-
-// In-register radix-2 DIF network (R <= 16): x[bitrev(k)] <- sum_r x_r e^{-2 pi i rk/R}
-template <int R>
-__device__ __forceinline__ void net_fwd(double2 (&x)[R]) {
-#pragma unroll
-  for (int span = R / 2; span >= 1; span >>= 1) {
-#pragma unroll
-    for (int b = 0; b < R; b += 2 * span) {
-#pragma unroll
-      for (int j = 0; j < span; j++) {
-        const double2 u = x[b + j], v = x[b + j + span];
-        x[b + j] = cadd(u, v);
-        x[b + j + span] = rot16<false>(csub(u, v), j * (8 / span));  // W_{2 span}^j
-      }
-    }
-  }
-}
-// exact inverse (unnormalised): natural order out of bit-reversed registers
-template <int R>
-__device__ __forceinline__ void net_inv(double2 (&x)[R]) {
-#pragma unroll
-  for (int span = 1; span <= R / 2; span <<= 1) {
-#pragma unroll
-    for (int b = 0; b < R; b += 2 * span) {
-#pragma unroll
-      for (int j = 0; j < span; j++) {
-        const double2 v = rot16<true>(x[b + j + span], j * (8 / span));
-        const double2 u = x[b + j];
-        x[b + j] = cadd(u, v);
-        x[b + j + span] = csub(u, v);
-      }
-    }
-  }
-}
-
-template <int R>
-__device__ __forceinline__ int brev(int k) {
-  int r = 0;
-#pragma unroll
-  for (int b = 1; b < R; b <<= 1) r = (r << 1) | ((k & b) ? 1 : 0);
-  return r;
-}
-
-// w[k] = w1^k, k < R, by a product tree (dependency depth log2 R instead of R)
-template <int R>
-__device__ __forceinline__ void powers(double2 (&w)[R], double2 w1) {
-  w[0] = make_double2(1.0, 0.0);
-  if (R > 1) w[1] = w1;
-#pragma unroll
-  for (int k = 2; k < R; k++) w[k] = cmul(w[k / 2], w[k - k / 2]);
-}
-
-// ------------------------------------------------------------ schedule
-// Compile-time plan for H = 2^LOGH: NP passes of radix <= 16 (outer first),
-// TEAM threads per row (one radix-16 butterfly each), NR rows in flight per
-// 512-thread CTA, each team with its own buffer and named barrier.
-template <int LOGH>
-struct Cfg {
-  static constexpr int H = 1 << LOGH;
-  static constexpr int M = 2 * H;
-  static constexpr int NP = (LOGH + 3) / 4;
-  static constexpr int TEAM = (H / 16) < 32 ? 32 : ((H / 16) > kT ? kT : (H / 16));
-  static constexpr int NR = kT / TEAM;
-  static constexpr int lr(int p) { return LOGH / NP + (p < LOGH - (LOGH / NP) * NP ? 1 : 0); }
-  static constexpr int n_at(int p) {  // sub-length of DIF pass p
-    int n = H;
-    for (int q = 0; q < p; q++) n >>= lr(q);
-    return n;
-  }
-};
-
-template <int TEAM>
-__device__ __forceinline__ void team_sync(int team) {
-  if (TEAM <= 32)
-    __syncwarp();
-  else
-    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(TEAM) : "memory");
-}
-
-// Storage order of the precomputed spectra: the fused innermost pass (radix R,
-// butterfly b = lt + q*TEAM reads positions b*R + k) finds its R values at
-// (q*R + k)*TEAM + lt, so each warp-wide load is one contiguous 512-byte run
-// instead of 32 lines 128 bytes apart.  Natural order when a team has idle
-// lanes (H/R < TEAM).
-template <int H, int R, int TEAM>
-__host__ __device__ constexpr int spec_index(int b, int k, int lt) {
-  return ((H / R) % TEAM == 0) ? (b - lt) * R + k * TEAM + lt : b * R + k;
-}
-
-// One radix-R pass on sub-length n (stride s = n/R), compile-time shape.  MODE:
-//   0 DIF   (load via LD, butterfly, twiddle, store via ST)
-//   1 DIT   (load, untwiddle, inverse butterfly, store)
-//   2 fused innermost DIF + spectrum multiply + innermost DIT (s = 1, j = 0)
-template <int R, int MODE, int H, int M, int n, int TEAM, class LD, class ST>
-__device__ __forceinline__ void pass(const double2* tw, const double2* spec, int lt, LD ld, ST st) {
-  constexpr int s = n / R, nb = H / R, tstep = M / n;
-  // one butterfly per thread when nb == TEAM (H = 8192): no unrolled copy (code size)
-  constexpr int UNR = nb > TEAM ? 2 : 1;
-#pragma unroll UNR
-  for (int b = lt; b < nb; b += TEAM) {
-    const int blk = b / s, j = b - blk * s, base = blk * n + j;
-    double2 x[R];
-    if (MODE == 0) {
-#pragma unroll
-      for (int r = 0; r < R; r++) x[r] = ld(base + r * s);
-      double2 w[R];
-      powers<R>(w, omega(tw, j * tstep, M));
-      net_fwd<R>(x);
-      st(base, x[0]);
-#pragma unroll
-      for (int k = 1; k < R; k++) st(base + k * s, cmul(x[brev<R>(k)], w[k]));
-    } else if (MODE == 1) {
-      double2 w[R];
-      powers<R>(w, omega(tw, j * tstep, M));
-      x[0] = ld(base);
-#pragma unroll
-      for (int k = 1; k < R; k++) x[brev<R>(k)] = cmulc(ld(base + k * s), w[k]);
-      net_inv<R>(x);
-#pragma unroll
-      for (int r = 0; r < R; r++) st(base + r * s, x[r]);
-    } else {
-      // spectra are stored thread-major (spec_index): a warp's loads coalesce
-      double2 sp[R];
-#pragma unroll
-      for (int k = 0; k < R; k++) sp[k] = spec[spec_index<H, R, TEAM>(b, k, lt)];
-#pragma unroll
-      for (int r = 0; r < R; r++) x[r] = ld(base + r);
-      net_fwd<R>(x);
-#pragma unroll
-      for (int k = 0; k < R; k++) x[brev<R>(k)] = cmul(x[brev<R>(k)], sp[k]);
-      net_inv<R>(x);
-#pragma unroll
-      for (int r = 0; r < R; r++) st(base + r, x[r]);
-    }
-  }
-}
-
-template <int LOGH, int P, class IN, class LDS, class STS>
-__device__ __forceinline__ void dif_chain(const double2* tw, int lt, int team, IN in, LDS lds,
-                                          STS sts) {
-  using C = Cfg<LOGH>;
-  if constexpr (P < C::NP - 1) {
-    constexpr int R = 1 << C::lr(P), n = C::n_at(P);
-    if constexpr (P == 0)
-      pass<R, 0, C::H, C::M, n, C::TEAM>(tw, nullptr, lt, in, sts);
-    else
-      pass<R, 0, C::H, C::M, n, C::TEAM>(tw, nullptr, lt, lds, sts);
-    team_sync<C::TEAM>(team);
-    dif_chain<LOGH, P + 1>(tw, lt, team, in, lds, sts);
-  }
-}
-
-template <int LOGH, int P, class OUT, class LDS, class STS>
-__device__ __forceinline__ void dit_chain(const double2* tw, int lt, int team, OUT out, LDS lds,
-                                          STS sts) {
-  using C = Cfg<LOGH>;
-  if constexpr (P >= 0) {
-    constexpr int R = 1 << C::lr(P), n = C::n_at(P);
-    if constexpr (P == 0)
-      pass<R, 1, C::H, C::M, n, C::TEAM>(tw, nullptr, lt, lds, out);
-    else
-      pass<R, 1, C::H, C::M, n, C::TEAM>(tw, nullptr, lt, lds, sts);
-    team_sync<C::TEAM>(team);
-    dit_chain<LOGH, P - 1>(tw, lt, team, out, lds, sts);
-  }
-}
-
-template <int LOGH, int P, class LDS, class STS>
-__device__ __forceinline__ void dit_mid(const double2* tw, int lt, int team, LDS lds, STS sts) {
-  using C = Cfg<LOGH>;
-  if constexpr (P >= 1) {
-    constexpr int R = 1 << C::lr(P), n = C::n_at(P);
-    pass<R, 1, C::H, C::M, n, C::TEAM>(tw, nullptr, lt, lds, sts);
-    team_sync<C::TEAM>(team);
-    dit_mid<LOGH, P - 1>(tw, lt, team, lds, sts);
-  }
-}
-
-// The passes between the first DIF pass and the last DIT pass touch only the
-// shared-memory row, so call sites with OUTLINE share ONE out-of-line copy of
-// them: k_theta_fwd (four half-convolutions per task) then fits the
-// instruction cache, which its fully inlined form (7 passes per call site,
-// ~2.7k instructions each) did not.  Kernels with two call sites keep the
-// inlined form (the call costs ~3% there).
-template <int LOGH>
-__device__ __noinline__ void conv_middle(double2* X, const double2* tw, const double2* S, int lt,
-                                         int team) {
-  using C = Cfg<LOGH>;
-  auto lds = [&](int i) { return X[phys(i)]; };
-  auto sts = [&](int i, double2 v) { X[phys(i)] = v; };
-  constexpr int RL = 1 << C::lr(C::NP - 1), nL = C::n_at(C::NP - 1);
-  dif_chain<LOGH, 1>(tw, lt, team, lds, lds, sts);
-  pass<RL, 2, C::H, C::M, nL, C::TEAM>(tw, S, lt, lds, sts);
-  team_sync<C::TEAM>(team);
-  dit_mid<LOGH, C::NP - 2>(tw, lt, team, lds, sts);
-}
-
-// z = DIT_H( DIF_H(x) . S ), x from IN(j), z delivered to OUT(k, z_k) (unnormalised).
-// The first DIF pass reads IN, the innermost DIF pass + spectrum multiply +
-// innermost DIT pass are one register pass, the last DIT pass hands results to OUT.
-template <int LOGH, bool OUTLINE = false, class IN, class OUT>
-__device__ __forceinline__ void conv_half(double2* X, const double2* tw, const double2* S, int lt,
-                                          int team, IN in, OUT out) {
-  using C = Cfg<LOGH>;
-  auto lds = [&](int i) { return X[phys(i)]; };
-  auto sts = [&](int i, double2 v) { X[phys(i)] = v; };
-  team_sync<C::TEAM>(team);
-  constexpr int RL = 1 << C::lr(C::NP - 1), nL = C::n_at(C::NP - 1);
-  if constexpr (C::NP == 1) {
-    pass<RL, 2, C::H, C::M, nL, C::TEAM>(tw, S, lt, in, out);
-    team_sync<C::TEAM>(team);
-  } else {
-    if constexpr (OUTLINE) {
-      constexpr int R0 = 1 << C::lr(0);
-      pass<R0, 0, C::H, C::M, C::H, C::TEAM>(tw, nullptr, lt, in, sts);
-      team_sync<C::TEAM>(team);
-      conv_middle<LOGH>(X, tw, S, lt, team);
-      pass<R0, 1, C::H, C::M, C::H, C::TEAM>(tw, nullptr, lt, lds, out);
-      team_sync<C::TEAM>(team);
-    } else {
-      dif_chain<LOGH, 0>(tw, lt, team, in, lds, sts);
-      pass<RL, 2, C::H, C::M, nL, C::TEAM>(tw, S, lt, lds, sts);
-      team_sync<C::TEAM>(team);
-      dit_chain<LOGH, C::NP - 2>(tw, lt, team, out, lds, sts);
-    }
-  }
-}
-
-__device__ __forceinline__ void load_tw(double2* tws, const FftArgs& a) {
-  for (int i = threadIdx.x; i <= a.M / 4; i += kT) tws[i] = a.tw[i];
-  __syncthreads();
-}
-
-__device__ __forceinline__ int fbin(int k, int N) { return k >= 0 ? k : k + N; }
-
-// Bluestein DFT_N of x (fx(n), n < N): forward (conj chirp, spec f) or inverse
-// (chirp, spec i).  Half 1 leaves z1 in scr; half 0 calls fin(k, y_k) with the
-// merged y[k] = z0[k] + w^-k z1[k] (unnormalised; DFT = chirp' . y / M).
-template <int LOGH, bool INV, bool OUTLINE = false, class FX, class FIN>
-__device__ __forceinline__ void bluestein(double2* X, const double2* tw, double2* scr,
-                                          const FftArgs& a, int lt, int team, FX fx, FIN fin) {
-  using C = Cfg<LOGH>;
-  const double2* spec = INV ? a.speci : a.specf;
-  const int N = a.N;
-  auto in1 = [&](int j) {
-    double2 v = make_double2(0.0, 0.0);
-    if (j < N) {
-      const double2 c = a.chirp[j];
-      v = INV ? cmul(fx(j), c) : cmulc(fx(j), c);
-      v = cmul(v, omega(tw, j, C::M));
-    }
-    return v;
-  };
-  auto in0 = [&](int j) {
-    double2 v = make_double2(0.0, 0.0);
-    if (j < N) {
-      const double2 c = a.chirp[j];
-      v = INV ? cmul(fx(j), c) : cmulc(fx(j), c);
-    }
-    return v;
-  };
-  auto out1 = [&](int k, double2 v) { scr[k] = v; };
-  auto out0 = [&](int k, double2 v) { fin(k, cadd(v, cmulc(scr[k], omega(tw, k, C::M)))); };
-  conv_half<LOGH, OUTLINE>(X, tw, spec + C::H, lt, team, in1, out1);
-  conv_half<LOGH, OUTLINE>(X, tw, spec, lt, team, in0, out0);
-}
-
-// Per-CTA setup shared by the stage kernels: team split, buffers, twiddles.
-#define FFT_PROLOGUE                                                         \
-  pdl_trigger();                                                             \
-  using C = Cfg<LOGH>;                                                       \
-  extern __shared__ __align__(16) double2 sm[];                              \
-  const int team = threadIdx.x / C::TEAM, lt = threadIdx.x - team * C::TEAM; \
-  double2* X = sm + team * C::H;                                             \
-  double2* tws = sm + C::NR * C::H;                                          \
-  load_tw(tws, a);                                                           \
-  pdl_wait(); /* every access below touches the previous stage's output */   \
-  double2* scr = a.scratch + ((long long)blockIdx.x * C::NR + team) * 3 * C::H;
-
-// ------------------------------------------------------------------ kernels
-
-// phi DFT of each ring (forward): AT[k][t] = (2 pi/N) sum_p f[t][p] e^{-2 pi i kp/N}
-// complex: k < N, AT is (N, L); real: k < L (rfft bins), AT is (L, L).
-// Real rings go two per transform: z = f_t + i f_{t+1}, Z = DFT_N(z), then
-// F_t[k] = (Z[k] + conj Z[N-k]) / 2 and F_{t+1}[k] = (Z[k] - conj Z[N-k]) / 2i.
-template <bool REAL, int LOGH>
-__global__ void __launch_bounds__(kT, 1) k_phi_fwd(FftArgs a) {
-  FFT_PROLOGUE
-  const int L = a.L, N = a.N;
-  const int kout = REAL ? L : N;
-  const double sc = 2.0 * 3.141592653589793 / (double)N / (double)C::M;
-  const int per_map = REAL ? (a.nrows + 1) / 2 : a.nrows;  // transforms per map
-  for (int row = blockIdx.x * C::NR + team; row < per_map * a.nmaps; row += gridDim.x * C::NR) {
-    const int map = row / per_map, q = row - map * per_map;
-    double2* at = (double2*)a.out + (long long)map * a.out_stride;
-    if (REAL) {
-      const int tl = 2 * q, t = a.t0 + tl;
-      const bool two = tl + 1 < a.nrows;
-      const double* f = (const double*)a.in + (long long)map * a.in_stride + (long long)tl * N;
-      const double* f2 = two ? f + N : f;
-      bluestein<LOGH, false>(
-          X, tws, scr, a, lt, team,
-          [&](int n) { return make_double2(f[n], two ? f2[n] : 0.0); },
-          [&](int k, double2 y) {
-            if (k < N) X[phys(k)] = cmulc(y, a.chirp[k]);
-          });
-      team_sync<C::TEAM>(team);
-      const double h = 0.5 * sc;
-      for (int k = lt; k < L; k += C::TEAM) {
-        const double2 zk = X[phys(k)], zn = X[phys(k ? N - k : 0)];
-        at[(long long)k * L + t] = make_double2(h * (zk.x + zn.x), h * (zk.y - zn.y));
-        if (two) at[(long long)k * L + t + 1] = make_double2(h * (zk.y + zn.y), h * (zn.x - zk.x));
-      }
-      team_sync<C::TEAM>(team);
-    } else {
-      const int tl = q, t = a.t0 + tl;
-      auto fin = [&](int k, double2 y) {
-        if (k < kout) at[(long long)k * L + t] = cscale(cmulc(y, a.chirp[k]), sc);
-      };
-      const double2* f = (const double2*)a.in + (long long)map * a.in_stride + (long long)tl * N;
-      bluestein<LOGH, false>(X, tws, scr, a, lt, team, [&](int n) { return f[n]; }, fin);
-    }
-  }
-}
-
-// Inverse theta rows go two per Bluestein transform.  Row m's synthesis
-// output is a reflection about t = L-1 with sign eps_m = (-1)^(m+s)
-// (F_{m,-m'} = eps_m F_{m,m'}, mw.py:400-401), and consecutive orders m, m+1
-// have opposite signs, so the transform of S_1 + i S_2 separates exactly:
-// z = y_1 + i y_2 and eps_1 z[N-1-t] = y_1[t] - i y_2[t].
-// Tasks pair the orders of magnitude 2k and 2k+1 within the +m block and
-// within the -m block, so a sharded order range [m0, m1) with even bounds
-// pairs exactly as the whole plane does (bit-identical shards).
-__device__ __forceinline__ int pair_count(int lo, int hi) {  // k with [2k, 2k+1] meeting [lo, hi)
-  return hi > lo ? (hi - 1) / 2 - lo / 2 + 1 : 0;
-}
-__device__ __forceinline__ int theta_tasks(int m0, int m1, bool real) {
-  return pair_count(m0, m1) + (real ? 0 : pair_count(m0 > 0 ? m0 : 1, m1));
-}
-// rows of task q: i1 and, when it returns 2, i1 + 1 (row_order indexing)
-__device__ __forceinline__ int theta_task(int q, int m0, int m1, bool real, int& i1) {
-  const int tp = pair_count(m0, m1);
-  int lo = m0, off = 0;
-  if (!real && q >= tp) {
-    q -= tp;
-    lo = m0 > 0 ? m0 : 1;
-    off = m1 - m0;
-  }
-  const int k = lo / 2 + q;
-  const int first = max(2 * k, lo), last = min(2 * k + 1, m1 - 1);
-  i1 = off + (first - lo);
-  return last - first + 1;
-}
-
-// theta stage of the forward transform for each order row (m from row_order):
-// extension (mw.py:161-177), DFT_N + twist (:180-192), weight correlation
-// (:244-251) and m' fold (:273-285, 504-511), written in the forward core's
-// staging layout gfT (ldw columns, +m / -m halves).  Two rows per Bluestein
-// transform: the extended sequence x of order m satisfies x[N-1-n] = eps_m x[n]
-// except at the self-mirrored n = L-1, so its DFT obeys
-//   Z[-k] e^{2 pi i k/N} = eps_m Z[k] + (1 - eps_m) x[L-1] (-1)^k e^{i pi k/N},
-// and with eps_{m+1} = -eps_m the transform of x_m + i x_{m+1} separates.
-template <bool REAL, int LOGH>
-__global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
-  FFT_PROLOGUE
-  double2* scrF[2] = {scr + C::H, scr + 2 * C::H};  // F of the task's rows (N <= H)
-  const int L = a.L, N = a.N, ldw = a.ldw;
-  constexpr int H = C::H, M = C::M;
-  // Two rows per transform from H = 2048 (L >= 1024) on, where the rows
-  // outnumber the teams; below, every row gets its own team in one wave and
-  // the shorter unpaired task (4 instead of 6 half-convolutions) wins
-  // (L=64: 79 -> 46 us, L=256: 128 -> 74 us per launch).
-  constexpr bool PAIR = LOGH >= 11;
-  const int ntask = PAIR ? theta_tasks(a.m0, a.m1, REAL) : a.nrows;
-  for (int task = blockIdx.x * C::NR + team; task < ntask * a.nmaps; task += gridDim.x * C::NR) {
-    const int map = task / ntask, q = task - map * ntask;
-    int i1 = q;
-    const bool two = PAIR && theta_task(q, a.m0, a.m1, REAL, i1) == 2;
-    int mr[2];
-    double eps[2];
-    const double2* g[2];
-    for (int u = 0; u < 2; u++) {
-      mr[u] = row_order(two ? i1 + u : i1, a.m0, a.m1, REAL);
-      eps[u] = (((mr[u] + (REAL ? 0 : a.spin)) & 1) ? -1.0 : 1.0);
-      g[u] = (const double2*)a.in + (long long)map * a.in_stride +
-             (long long)(REAL ? mr[u] : fbin(mr[u], N)) * L;
-    }
-    // 1. Bluestein DFT_N of the periodic extension(s): X[k] = M Z[k]
-    auto ext = [&](int u, int n) { return n < L ? g[u][n] : cscale(g[u][2 * L - 2 - n], eps[u]); };
-    bluestein<LOGH, false, PAIR>(
-        X, tws, scr, a, lt, team,
-        [&](int n) {
-          const double2 x1 = ext(0, n);
-          if (!two) return x1;
-          const double2 x2 = ext(1, n);
-          return make_double2(x1.x - x2.y, x1.y + x2.x);  // x1 + i x2
-        },
-        [&](int k, double2 y) {
-          if (k < N) X[phys(k)] = cmulc(y, a.chirp[k]);
-        });
-    team_sync<C::TEAM>(team);
-    // 2. separate the two rows; F[k] = Z[k] tau(f(k)) / (2 pi N)
-    {
-      double2 cc = make_double2(0.0, 0.0);  // M (1 - eps_u) x_u[L-1] (i for the second row)
-      if (two) {
-        const double2 c1 = g[0][L - 1], c2 = g[1][L - 1];
-        cc = eps[0] < 0 ? make_double2(2.0 * M * c1.x, 2.0 * M * c1.y)
-                        : make_double2(-2.0 * M * c2.y, 2.0 * M * c2.x);
-      }
-      // four elements per thread and pass: the table loads (L2) of a pass are in flight together
-      constexpr int U = 4;
-      for (int k0 = lt; k0 < N; k0 += U * C::TEAM) {
-        double2 r2[U], wk[U], ck[U];
-#pragma unroll
-        for (int v = 0; v < U; v++) {
-          const int k = min(k0 + v * C::TEAM, N - 1);
-          r2[v] = __ldg(&a.rho2[k]);
-          if (two) {
-            wk[v] = __ldg(&a.wnk[k]);
-            ck[v] = __ldg(&a.cen[k]);
-          }
-        }
-#pragma unroll
-        for (int v = 0; v < U; v++) {
-          const int k = k0 + v * C::TEAM;
-          if (k >= N) break;
-          const double2 zk = X[phys(k)];
-          if (!two) {
-            scrF[0][k] = cmul(zk, r2[v]);
-            continue;
-          }
-          const double2 zn = X[phys(k ? N - k : 0)];
-          const double2 bk = csub(cmul(zn, wk[v]), cmul(cc, ck[v]));
-          const double2 eb = cscale(bk, eps[0]);
-          const double2 s1 = cadd(zk, eb), s2 = csub(zk, eb);  // 2 Z_1, 2i Z_2
-          scrF[0][k] = cscale(cmul(s1, r2[v]), 0.5);
-          scrF[1][k] = cscale(cmul(make_double2(s2.y, -s2.x), r2[v]), 0.5);
-        }
-      }
-    }
-    team_sync<C::TEAM>(team);
-    for (int u = 0; u < (two ? 2 : 1); u++) {
-      const double2* F = scrF[u];
-      const int m = mr[u];
-      const bool neg = !REAL && m < 0;
-      const int am = neg ? -m : m;
-      // 3. weight correlation on F placed in FFT order (f at f mod M)
-      auto Fpl = [&](int p) -> double2 {
-        if (p < L) return F[p];
-        if (p >= M - L + 1) return F[p - M + N];
-        return make_double2(0.0, 0.0);
-      };
-      conv_half<LOGH, PAIR>(
-          X, tws, a.specw + H, lt, team,
-          [&](int j) { return cmul(csub(Fpl(j), Fpl(j + H)), omega(tws, j, M)); },
-          [&](int k, double2 v) { scr[k] = v; });
-      conv_half<LOGH, PAIR>(
-          X, tws, a.specw, lt, team, [&](int j) { return cadd(Fpl(j), Fpl(j + H)); },
-          [&](int k, double2 v) { X[phys(k)] = v; });
-      team_sync<C::TEAM>(team);
-      // 4. G(m') = y[m' mod M]/M; fold gf[j] = G(j) + s G(-j); write staging column
-      const double sig = eps[u];  // (-1)^(m+s) (complex) / (-1)^m (real), mw.py:273-285
-      const double inv = 1.0 / (double)M;
-      double2* gT =
-          (double2*)a.out + (long long)map * a.out_stride + (neg ? (long long)L * ldw : 0);
-      for (int j = lt; j < L; j += C::TEAM) {
-        double2 v = cadd(X[phys(j)], cmulc(scr[j], omega(tws, j, M)));
-        if (j > 0) {
-          const int k = H - j;  // position M - j = k + H
-          const double2 w = csub(X[phys(k)], cmulc(scr[k], omega(tws, k, M)));
-          v = make_double2(v.x + sig * w.x, v.y + sig * w.y);
-        }
-        v = cscale(v, inv);
-        if (neg && (j & 1)) v = make_double2(-v.x, -v.y);
-        gT[blk<kTileCols>(j, am, L)] = v;
-        if (!REAL && m == 0)
-          gT[(long long)L * ldw + blk<kTileCols>(j, 0, L)] = (j & 1) ? make_double2(-v.x, -v.y) : v;
-      }
-      team_sync<C::TEAM>(team);
-    }
-  }
-}
-
-// inverse theta synthesis per order row: rows[t] = sum_m' S[bin(m')] e^{+2 pi i m' t/N}
-// (S already carries the core's twist), keep t < L, write Out[t][col].
-template <bool REAL, int LOGH>
-__global__ void __launch_bounds__(kT, 1) k_theta_inv(FftArgs a) {
-  FFT_PROLOGUE
-  const int L = a.L, N = a.N;
-  const int ocols = REAL ? L : N;
-  const double inv = 1.0 / (double)C::M;
-  const int ntask = theta_tasks(a.m0, a.m1, REAL);
-  for (int task = blockIdx.x * C::NR + team; task < ntask * a.nmaps; task += gridDim.x * C::NR) {
-    const int map = task / ntask, q = task - map * ntask;
-    int i1;
-    const bool two = theta_task(q, a.m0, a.m1, REAL, i1) == 2;
-    int mr[2], col[2];
-    const double2* sp[2];
-    for (int u = 0; u < 2; u++) {
-      mr[u] = row_order(two ? i1 + u : i1, a.m0, a.m1, REAL);
-      const int r = REAL ? mr[u] : mr[u] + (L - 1);  // plane row of order m
-      sp[u] = (const double2*)a.in + (long long)map * a.in_stride + (long long)r * N;
-      col[u] = REAL ? mr[u] : fbin(mr[u], N);
-    }
-    const double e1 = (((mr[0] + (REAL ? 0 : a.spin)) & 1) ? -1.0 : 1.0);
-    double2* o = (double2*)a.out + (long long)map * a.out_stride;
-    bluestein<LOGH, true>(
-        X, tws, scr, a, lt, team,
-        [&](int n) {
-          const double2 s1 = sp[0][n];
-          if (!two) return s1;
-          const double2 s2 = sp[1][n];
-          return make_double2(s1.x - s2.y, s1.y + s2.x);  // S_1 + i S_2
-        },
-        [&](int t, double2 y) {
-          if (t < N) X[phys(t)] = cscale(cmul(y, a.chirp[t]), inv);
-        });
-    team_sync<C::TEAM>(team);
-    for (int t = lt; t < L; t += C::TEAM) {
-      const double2 z = X[phys(t)];
-      double2 v1 = z;
-      if (two) {
-        const double2 zr = cscale(X[phys(N - 1 - t)], e1);
-        v1 = cscale(cadd(z, zr), 0.5);
-        const double2 w = csub(z, zr);  // 2i y_2
-        o[(long long)t * ocols + col[1]] = make_double2(0.5 * w.y, -0.5 * w.x);
-      }
-      if (REAL && mr[0] == 0) v1.y = 0.0;  // irfft ignores Im of the DC bin
-      o[(long long)t * ocols + col[0]] = v1;
-    }
-    team_sync<C::TEAM>(team);
-  }
-}
-
-// inverse phi synthesis per ring t: samples[t][p] = sum_m Out[t][bin(m)] e^{+2 pi i m p/N}
-// (real: Hermitian completion of the m >= 0 half, real part out; mw.py:558).
-// Real rings go two per transform: IDFT(X_t + i X_{t+1}) = x_t + i x_{t+1}.
-template <bool REAL, int LOGH>
-__global__ void __launch_bounds__(kT, 1) k_phi_inv(FftArgs a) {
-  FFT_PROLOGUE
-  const int L = a.L, N = a.N;
-  const double inv = 1.0 / (double)C::M;
-  const int per_map = REAL ? (a.nrows + 1) / 2 : a.nrows;  // transforms per map
-  for (int row = blockIdx.x * C::NR + team; row < per_map * a.nmaps; row += gridDim.x * C::NR) {
-    const int map = row / per_map, q = row - map * per_map;
-    if (REAL) {
-      const int tl = 2 * q, t = a.t0 + tl;
-      const bool two = tl + 1 < a.nrows;
-      const double2* h = (const double2*)a.in + (long long)map * a.in_stride + (long long)t * L;
-      const double2* h2 = h + L;
-      double* o = (double*)a.out + (long long)map * a.out_stride + (long long)tl * N;
-      bluestein<LOGH, true>(
-          X, tws, scr, a, lt, team,
-          [&](int n) {
-            const double2 x1 = n < L ? h[n] : conjd(h[N - n]);
-            if (!two) return x1;
-            const double2 x2 = n < L ? h2[n] : conjd(h2[N - n]);
-            return make_double2(x1.x - x2.y, x1.y + x2.x);  // x1 + i x2
-          },
-          [&](int p, double2 y) {
-            if (p < N) {
-              const double2 v = cmul(y, a.chirp[p]);
-              o[p] = v.x * inv;
-              if (two) o[N + p] = v.y * inv;
-            }
-          });
-    } else {
-      const int tl = q, t = a.t0 + tl;
-      const double2* h = (const double2*)a.in + (long long)map * a.in_stride + (long long)t * N;
-      double2* o = (double2*)a.out + (long long)map * a.out_stride + (long long)tl * N;
-      bluestein<LOGH, true>(X, tws, scr, a, lt, team, [&](int n) { return h[n]; },
-                            [&](int p, double2 y) {
-                              if (p < N) o[p] = cscale(cmul(y, a.chirp[p]), inv);
-                            });
-    }
-  }
-}
-
-// plan time: S_0 = DIF_H(k[j] + k[j+H]), S_1 = DIF_H((k[j] - k[j+H]) w^j) of a
-// natural-order length-M kernel k, in the digit-reversed layout conv_half uses
-// (every DIF pass including the innermost one, no spectrum).  One team.
-template <int LOGH, int P, class LDS, class STS>
-__device__ __forceinline__ void dif_all(const double2* tw, int lt, LDS lds, STS sts) {
-  using C = Cfg<LOGH>;
-  if constexpr (P < C::NP) {
-    constexpr int R = 1 << C::lr(P), n = C::n_at(P);
-    pass<R, 0, C::H, C::M, n, C::TEAM>(tw, nullptr, lt, lds, sts);
-    team_sync<C::TEAM>(0);
-    dif_all<LOGH, P + 1>(tw, lt, lds, sts);
-  }
-}
-
-template <int LOGH>
-__global__ void __launch_bounds__(kT, 1) k_spectrum(FftArgs a, const double2* kern, double2* spec) {
-  FFT_PROLOGUE
-  (void)scr;
-  if (team != 0) return;
-  auto lds = [&](int i) { return X[phys(i)]; };
-  auto sts = [&](int i, double2 v) { X[phys(i)] = v; };
-  for (int half = 0; half < 2; half++) {
-    for (int j = lt; j < C::H; j += C::TEAM) {
-      const double2 u = kern[j], v = kern[j + C::H];
-      X[phys(j)] = half ? cmul(csub(u, v), omega(tws, j, C::M)) : cadd(u, v);
-    }
-    team_sync<C::TEAM>(0);
-    dif_all<LOGH, 0>(tws, lt, lds, sts);
-    constexpr int RL = 1 << C::lr(C::NP - 1);
-    for (int j = lt; j < C::H; j += C::TEAM) {
-      const int b = j / RL, k = j - b * RL;
-      spec[half * C::H + spec_index<C::H, RL, C::TEAM>(b, k, b % C::TEAM)] = X[phys(j)];
-    }
-    team_sync<C::TEAM>(0);
-  }
-}
-
-template <int LOGH>
-size_t smem_bytes_t() {
-  using C = Cfg<LOGH>;
-  return sizeof(double2) * ((size_t)C::NR * C::H + C::M / 4 + 1);
-}
-
-template <int LOGH, class K>
-static void launch_t(K kern, const FftArgs& a, int nsm, cudaStream_t st) {
-  using C = Cfg<LOGH>;
-  const size_t sm = smem_bytes_t<LOGH>();
-  smem_attr_once((const void*)kern, sm);
-  long long rows = (long long)a.nrows * a.nmaps;
-  long long grid = (rows + C::NR - 1) / C::NR;
-  // resident CTAs per SM, within the per-SM scratch budget (NR * H * occ <= 8192)
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kT, sm);
-  if (occ < 1) occ = 1;
-  if (occ * C::NR * C::H > 8192) occ = 8192 / (C::NR * C::H);
-  if (grid > (long long)nsm * occ) grid = (long long)nsm * occ;
-  if (grid < 1) grid = 1;
-  launch_pdl(kern, dim3((unsigned)grid), dim3(kT), sm, st, a);
-}
-
-template <int LOGH>
-static void launch_stage(int which, bool real, const FftArgs& a, int nsm, cudaStream_t st) {
-  switch (which) {
-    case 0:
-      real ? launch_t<LOGH>(k_phi_fwd<true, LOGH>, a, nsm, st)
-           : launch_t<LOGH>(k_phi_fwd<false, LOGH>, a, nsm, st);
-      break;
-    case 1:
-      real ? launch_t<LOGH>(k_theta_fwd<true, LOGH>, a, nsm, st)
-           : launch_t<LOGH>(k_theta_fwd<false, LOGH>, a, nsm, st);
-      break;
-    case 2:
-      real ? launch_t<LOGH>(k_theta_inv<true, LOGH>, a, nsm, st)
-           : launch_t<LOGH>(k_theta_inv<false, LOGH>, a, nsm, st);
-      break;
-    default:
-      real ? launch_t<LOGH>(k_phi_inv<true, LOGH>, a, nsm, st)
-           : launch_t<LOGH>(k_phi_inv<false, LOGH>, a, nsm, st);
-      break;
-  }
-}
-
-template <int LOGH>
-static void spectrum_t(const FftArgs& a, const double2* kern, double2* spec, cudaStream_t st) {
-  const size_t sm = smem_bytes_t<LOGH>();
-  smem_attr_once((const void*)k_spectrum<LOGH>, sm);
-  k_spectrum<LOGH><<<1, kT, sm, st>>>(a, kern, spec);
-}
 
 #define MWSHT_FFT_SIZES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13)
 
-}  // namespace fft
+namespace mwsht {
+#define DECL(k)                                                                           \
+  void fft_launch_##k(int which, bool real, const fft::FftArgs& a, int nsm, cudaStream_t st); \
+  void fft_spectrum_##k(const fft::FftArgs& a, const double2* kern, double2* spec, cudaStream_t st);
+MWSHT_FFT_SIZES(DECL)
+#undef DECL
 
-using fft::FftArgs;
-
-void fft_launch(int which, bool real, const FftArgs& a, int nsm, cudaStream_t st) {
+void fft_launch(int which, bool real, const fft::FftArgs& a, int nsm, cudaStream_t st) {
   switch (a.logH) {
-#define CASE(k) \
-  case k:       \
-    fft::launch_stage<k>(which, real, a, nsm, st); \
+#define CASE(k)                              \
+  case k:                                    \
+    fft_launch_##k(which, real, a, nsm, st); \
     break;
     MWSHT_FFT_SIZES(CASE)
 #undef CASE
   }
 }
 
-void fft_spectrum(const FftArgs& a, const double2* kern, double2* spec, cudaStream_t st) {
+void fft_spectrum(const fft::FftArgs& a, const double2* kern, double2* spec, cudaStream_t st) {
   switch (a.logH) {
-#define CASE(k) \
-  case k:       \
-    fft::spectrum_t<k>(a, kern, spec, st); \
+#define CASE(k)                             \
+  case k:                                   \
+    fft_spectrum_##k(a, kern, spec, st);    \
     break;
     MWSHT_FFT_SIZES(CASE)
 #undef CASE

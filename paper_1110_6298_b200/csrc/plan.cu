@@ -23,7 +23,9 @@ void launch_fold(bool real, const double2* gf, double2* gfT, int L, int ldw, cud
 void launch_T2_to_fold(bool real, const double2* gfT, double2* gf, int L, int ldw, cudaStream_t st);
 void launch_inv_prescale(bool real, const double2* in, int in_mode, const double* cl,
                          const double* A, int L, int ldw, double2* gp, long long is, long long gs,
-                         int nm, cudaStream_t st);
+                         int nm, cudaStream_t st, int c0 = 0, int c1 = -1);
+void launch_flm_unpack(const double2* gathered, long long maxlen, const int* bounds, int world,
+                       int L, double2* flm, cudaStream_t st);
 void launch_reality(const double2* f, int L, unsigned long long* red, unsigned long long* host,
                     cudaStream_t st);
 void fft_launch(int which, bool real, const fft::FftArgs& a, int nsm, cudaStream_t st);
@@ -1063,8 +1065,8 @@ static int check_range(mwsht_plan* p, int m0, int m1) {
   return MWSHT_OK;
 }
 
-int mwsht_shard_forward_phi(mwsht_plan* p, const void* samples_rows, int t0, int t1, void* AT,
-                            void* stream) {
+int mwsht_shard_forward_phi(mwsht_plan* p, const void* samples_rows, int t0, int t1,
+                            const long long* row_off, void* out, void* stream) {
   DevGuard dg;
   int rc;
   if ((rc = check_plan(p, dg))) return rc;
@@ -1077,18 +1079,22 @@ int mwsht_shard_forward_phi(mwsht_plan* p, const void* samples_rows, int t0, int
   a.t0 = t0;
   a.in = samples_rows;
   a.in_stride = 0;
-  a.out = AT;
+  a.out = out;
   a.out_stride = 0;
+  a.row_off = row_off;
   fft_launch(0, false, a, p->nsm, (cudaStream_t)stream);
   LAUNCHED(p);
   return MWSHT_OK;
 }
 
-int mwsht_shard_forward_rest(mwsht_plan* p, const void* AT, int m0, int m1, int spin, void* flm,
-                             void* stream) {
+int mwsht_shard_forward_rest(mwsht_plan* p, const void* in, int m0, int m1,
+                             const long long* col_off, const int* col_stride, int spin, void* flm,
+                             int packed, void* stream) {
   DevGuard dg;
   int rc;
   if ((rc = check_plan(p, dg)) || (rc = check_spin(p, spin)) || (rc = check_range(p, m0, m1))) return rc;
+  if ((col_off == nullptr) != (col_stride == nullptr))
+    return fail(MWSHT_E_CONTRACT, "shard", "col_off and col_stride go together");
   std::lock_guard<std::mutex> lk(p->mu);
   StreamUse su(p, (cudaStream_t)stream);
   if ((rc = build_spin(p, spin))) return rc;
@@ -1101,16 +1107,20 @@ int mwsht_shard_forward_rest(mwsht_plan* p, const void* AT, int m0, int m1, int 
   a.m0 = m0;
   a.m1 = m1;
   a.nrows = 2 * (m1 - m0) - (m0 == 0 ? 1 : 0);
-  a.in = AT;
+  a.in = in;
   a.in_stride = 0;
   a.out = p->bufG;
   a.out_stride = p->strideG;
+  a.col_off = col_off;
+  a.col_stride = col_stride;
   fft_launch(1, false, a, p->nsm, st);
   LAUNCHED(p);
   FwdArgs f = fwd_args(p, spin);
   f.tiles = ts->fwd;
   f.out = (double2*)flm;
-  f.out_mode = 0;
+  f.out_mode = packed ? 2 : 0;
+  f.m0 = m0;
+  f.m1 = m1;
   f.out_stride = (long long)p->L * p->L;
   if (ts->nfwd) {
     launch_forward_core(f, ts->nfwd, 1, false, st);
@@ -1119,8 +1129,8 @@ int mwsht_shard_forward_rest(mwsht_plan* p, const void* AT, int m0, int m1, int 
   return MWSHT_OK;
 }
 
-int mwsht_shard_inverse_front(mwsht_plan* p, const void* flm, int m0, int m1, int spin, void* OUT,
-                              void* stream) {
+int mwsht_shard_inverse_front(mwsht_plan* p, const void* flm, int m0, int m1, int spin,
+                              const long long* row_off, void* out, void* stream) {
   DevGuard dg;
   int rc;
   if ((rc = check_plan(p, dg)) || (rc = check_spin(p, spin)) || (rc = check_range(p, m0, m1))) return rc;
@@ -1132,8 +1142,9 @@ int mwsht_shard_inverse_front(mwsht_plan* p, const void* flm, int m0, int m1, in
   p->own_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
   const int L = p->L, N = p->N;
+  // only the shard's staging columns (its tiles read nothing else)
   launch_inv_prescale(false, (const double2*)flm, 0, p->tabs.cl, p->tabs.A, L, p->ldw, p->bufG,
-                      (long long)L * L, p->strideG, 1, st);
+                      (long long)L * L, p->strideG, 1, st, m0, m1 == L ? p->ldw : m1);
   LAUNCHED(p);
   InvArgs a = inv_args(p, spin);
   a.paired = 0;  // order-restricted tiles: the transpose would leave the shard's orders
@@ -1152,30 +1163,51 @@ int mwsht_shard_inverse_front(mwsht_plan* p, const void* flm, int m0, int m1, in
   f.nrows = 2 * (m1 - m0) - (m0 == 0 ? 1 : 0);
   f.in = p->bufB;
   f.in_stride = 0;
-  f.out = OUT;
+  f.out = out;
   f.out_stride = 0;
+  f.row_off = row_off;
   fft_launch(2, false, f, p->nsm, st);
   LAUNCHED(p);
   return MWSHT_OK;
 }
 
-int mwsht_shard_inverse_phi(mwsht_plan* p, const void* OUT, int t0, int t1, void* samples_rows,
+int mwsht_shard_inverse_phi(mwsht_plan* p, const void* in, int t0, int t1,
+                            const long long* col_off, const int* col_stride, void* samples_rows,
                             void* stream) {
   DevGuard dg;
   int rc;
   if ((rc = check_plan(p, dg))) return rc;
   if (t0 < 0 || t1 > p->L || t0 >= t1) return fail(MWSHT_E_CONTRACT, "shard", "bad ring range");
+  if ((col_off == nullptr) != (col_stride == nullptr))
+    return fail(MWSHT_E_CONTRACT, "shard", "col_off and col_stride go together");
   std::lock_guard<std::mutex> lk(p->mu);
   StreamUse su(p, (cudaStream_t)stream);
   p->own_launches = 0;
   fft::FftArgs f = fft_args(p);
   f.nrows = t1 - t0;
   f.t0 = t0;
-  f.in = OUT;
+  f.in = in;
   f.in_stride = 0;
   f.out = samples_rows;
   f.out_stride = 0;
+  f.col_off = col_off;
+  f.col_stride = col_stride;
   fft_launch(3, false, f, p->nsm, (cudaStream_t)stream);
+  LAUNCHED(p);
+  return MWSHT_OK;
+}
+
+int mwsht_shard_unpack_flm(mwsht_plan* p, const void* gathered, long long maxlen,
+                           const int* bounds, int world, void* flm, void* stream) {
+  DevGuard dg;
+  int rc;
+  if ((rc = check_plan(p, dg))) return rc;
+  if (world < 1 || !bounds || !gathered || !flm)
+    return fail(MWSHT_E_CONTRACT, "shard_unpack_flm", "null buffer or world < 1");
+  std::lock_guard<std::mutex> lk(p->mu);
+  p->own_launches = 0;
+  launch_flm_unpack((const double2*)gathered, maxlen, bounds, world, p->L, (double2*)flm,
+                    (cudaStream_t)stream);
   LAUNCHED(p);
   return MWSHT_OK;
 }

@@ -69,11 +69,12 @@ __global__ void k_T2_to_fold(const double2* __restrict__ gfT, double2* __restric
 //   gp[blk32(l, m)] = c_l u_l(m) f_{l,m},  gn[blk32(l, m)] = (-1)^l c_l u_l(m) f_{l,-m},
 //   u_l(m) = A(l-m) A(l+m), zero for m > l.
 // in_mode 0: flat l(l+1)+m; 1: table (L, N) column L-1+m (real: (L, L) column m).
+// Columns c0 <= m < c1 only (an order-range shard's columns; full: 0, ldw).
 template <bool REAL>
 __global__ void k_inv_prescale(const double2* __restrict__ in, int in_mode,
                                const double* __restrict__ cl, const double* __restrict__ A, int L,
                                int ldw, double2* __restrict__ gp, long long in_stride,
-                               long long g_stride) {
+                               long long g_stride, int c0, int c1) {
   pdl_trigger();
   pdl_wait();  // reads the caller's coefficients, overwrites the core staging
   const int l = blockIdx.y;
@@ -81,7 +82,7 @@ __global__ void k_inv_prescale(const double2* __restrict__ in, int in_mode,
   const double2* f = in + (long long)blockIdx.z * in_stride;
   double2* p = gp + (long long)blockIdx.z * g_stride;
   double2* n = p + (long long)L * ldw;
-  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < ldw; m += gridDim.x * blockDim.x) {
+  for (int m = c0 + blockIdx.x * blockDim.x + threadIdx.x; m < c1; m += gridDim.x * blockDim.x) {
     double2 vp = make_double2(0.0, 0.0), vn = vp;
     if (m <= l) {
       const double u = cl[l] * A[l - m] * A[l + m];
@@ -134,7 +135,34 @@ __global__ void k_reality(const double2* __restrict__ f, int L, unsigned long lo
   }
 }
 
+// m-column sharding: the all-gathered packed coefficient blocks (one block of
+// `maxlen` entries per rank, shard_flm_index layout) -> flat flm.
+__global__ void k_flm_unpack(const double2* __restrict__ gathered, long long maxlen,
+                             const int* __restrict__ bounds, int world, int L,
+                             double2* __restrict__ flm) {
+  const long long n = (long long)L * L;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int l = (int)sqrt((double)idx);
+    while ((long long)l * l > idx) l--;
+    while ((long long)(l + 1) * (l + 1) <= idx) l++;
+    const int m = (int)(idx - (long long)l * (l + 1));
+    const int am = m < 0 ? -m : m;
+    int r = 0;
+    while (r + 1 < world && bounds[r + 1] <= am) r++;
+    flm[idx] = gathered[(long long)r * maxlen + shard_flm_index(l, m, bounds[r], bounds[r + 1])];
+  }
+}
+
 // ------------------------------------------------------------- launchers
+void launch_flm_unpack(const double2* gathered, long long maxlen, const int* bounds, int world,
+                       int L, double2* flm, cudaStream_t st) {
+  long long n = (long long)L * L;
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_flm_unpack<<<(unsigned)blocks, 256, 0, st>>>(gathered, maxlen, bounds, world, L, flm);
+}
+
 void launch_fold(bool real, const double2* gf, double2* gfT, int L, int ldw, cudaStream_t st) {
   dim3 grid((L + 31) / 32, ldw / 32, real ? 1 : 2), block(32, 8);
   if (real)
@@ -154,13 +182,16 @@ void launch_T2_to_fold(bool real, const double2* gfT, double2* gf, int L, int ld
 
 void launch_inv_prescale(bool real, const double2* in, int in_mode, const double* cl,
                          const double* A, int L, int ldw, double2* gp, long long is, long long gs,
-                         int nm, cudaStream_t st) {
+                         int nm, cudaStream_t st, int c0, int c1) {
+  if (c1 < 0) c1 = ldw;
   const int threads = 128;
-  dim3 grid((ldw + threads - 1) / threads, L, nm);
+  dim3 grid((c1 - c0 + threads - 1) / threads, L, nm);
   if (real)
-    launch_pdl(k_inv_prescale<true>, grid, threads, 0, st, in, in_mode, cl, A, L, ldw, gp, is, gs);
+    launch_pdl(k_inv_prescale<true>, grid, threads, 0, st, in, in_mode, cl, A, L, ldw, gp, is, gs,
+               c0, c1);
   else
-    launch_pdl(k_inv_prescale<false>, grid, threads, 0, st, in, in_mode, cl, A, L, ldw, gp, is, gs);
+    launch_pdl(k_inv_prescale<false>, grid, threads, 0, st, in, in_mode, cl, A, L, ldw, gp, is, gs,
+               c0, c1);
 }
 
 // Hands the two maxima to host-mapped memory with plain stores and re-zeroes the

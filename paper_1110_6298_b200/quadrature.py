@@ -123,7 +123,7 @@ def synthesize_reduced(coeffs, recursion="trapani"):
     N = 2 * L - 1
     rows = torch.empty((L, N), dtype=torch.complex128, device=f"cuda:{dev}")  # [t][bin(m)]
     plan = get_plan(L, dev)
-    _lib.check(_lib.load().mwsht_shard_inverse_front(plan.handle, f.data_ptr(), 0, L, int(spin),
+    _lib.check(_lib.load().mwsht_shard_inverse_front(plan.handle, f.data_ptr(), 0, L, int(spin), None,
                                                       rows.data_ptr(), _stream(dev)),
                "synthesize_reduced")
     k = torch.arange(N, device=rows.device)

@@ -66,40 +66,92 @@ def _run(fn, world=2):
     return dict(out)
 
 
-def _full_AT(L):
+def _spec(k, t):
+    """Synthetic spectrum value of bin k at ring t (distinct per pair)."""
+    return (k * 1000.0 + t) + 1j * (k - 0.5 * t)
+
+
+def _exchange_roundtrip(rank, world, L=200):
+    """Both all-to-all transposes through ExchangeLayout on real gloo ranks,
+    with numpy standing in for the stage kernels' table addressing
+    (include/mwsht.h): what the forward theta stage reads must be the phi
+    spectra of its orders for every ring, and what the inverse phi stage reads
+    must be every order's synthesis of its rings."""
     N = 2 * L - 1
-    k = torch.arange(N, dtype=torch.float64)[:, None]
-    t = torch.arange(L, dtype=torch.float64)[None, :]
-    return (k * 1000 + t) + 1j * (k - 0.5 * t)
-
-
-def _exchange_fwd(rank, world):
-    L = 70
     b = shard.balanced_m_splits(L, world, align=32)
     tb = shard.ring_splits(L, world)
-    full = _full_AT(L)
-    AT = torch.full_like(full, complex("nan"))
-    AT[:, tb[rank]:tb[rank + 1]] = full[:, tb[rank]:tb[rank + 1]]   # own rings only
-    shard.exchange_rings_to_orders(AT, b, tb, rank)
+    lay = shard.ExchangeLayout(L, b, tb, rank)
+    t0, t1 = tb[rank], tb[rank + 1]
     rows = shard.order_bins(L, b[rank], b[rank + 1])
-    return bool(torch.equal(AT[rows], full[rows]))
+    # forward: k_phi_fwd writes bin k, ring t at send[row_off[k] + t - t0]
+    send = torch.full((sum(lay.fsend_counts),), complex("nan"), dtype=torch.complex128)
+    for k in range(N):
+        for t in range(t0, t1):
+            send[lay.fphi_row_off[k] + t - t0] = _spec(k, t)
+    recv = torch.full((sum(lay.frecv_counts),), complex("nan"), dtype=torch.complex128)
+    shard.all_to_all_flat(send, lay.fsend_counts, recv, lay.frecv_counts)
+    ok = True
+    for i, k in enumerate(rows):   # k_theta_fwd reads row i, ring t
+        got = [recv[lay.ftheta_col_off[t] + i * lay.ftheta_col_stride[t]].item() for t in range(L)]
+        ok &= got == [_spec(k, t) for t in range(L)]
+    # inverse: k_theta_inv writes ring t of row i at send[row_off[t] + i]
+    isend = torch.full((sum(lay.isend_counts),), complex("nan"), dtype=torch.complex128)
+    for i, k in enumerate(rows):
+        for t in range(L):
+            isend[lay.itheta_row_off[t] + i] = _spec(k, t)
+    irecv = torch.full((sum(lay.irecv_counts),), complex("nan"), dtype=torch.complex128)
+    shard.all_to_all_flat(isend, lay.isend_counts, irecv, lay.irecv_counts)
+    for t in range(t0, t1):        # k_phi_inv reads ring t, bin n
+        got = [irecv[lay.iphi_col_off[n] + (t - t0) * lay.iphi_col_stride[n]].item()
+               for n in range(N)]
+        ok &= got == [_spec(n, t) for n in range(N)]
+    return bool(ok)
 
 
-def _exchange_inv(rank, world):
-    L = 70
+def _flm_gather(rank, world, L=150):
+    """Packed coefficient blocks (forward core out_mode 2) all-gathered and
+    unpacked (k_flm_unpack's index math, mirrored) rebuild the flat flm."""
     b = shard.balanced_m_splits(L, world, align=32)
-    tb = shard.ring_splits(L, world)
-    full = _full_AT(L).T.contiguous()   # (L, N)
-    OUT = torch.full_like(full, complex("nan"))
-    cols = shard.order_bins(L, b[rank], b[rank + 1])
-    OUT[:, cols] = full[:, cols]        # own orders only
-    shard.exchange_orders_to_rings(OUT, b, tb, rank)
-    return bool(torch.equal(OUT[tb[rank]:tb[rank + 1]], full[tb[rank]:tb[rank + 1]]))
+    lay = shard.ExchangeLayout(L, b, shard.ring_splits(L, world), rank)
+    full = np.arange(L * L) * (1.0 + 0.5j)
+    m0, m1 = b[rank], b[rank + 1]
+    block = torch.zeros(lay.flm_maxlen, dtype=torch.complex128)
+    n = 0
+    for l in range(L):
+        for m in range(-l, l + 1):
+            if m0 <= abs(m) < m1:
+                block[int(shard.shard_flm_index(l, m, m0, m1))] = complex(full[l * (l + 1) + m])
+                n += 1
+    assert n == lay.flm_len[rank]
+    gathered = torch.empty(world * lay.flm_maxlen, dtype=torch.complex128)
+    shard.all_gather_flat(block, gathered)
+    out = np.empty(L * L, complex)
+    for l in range(L):
+        for m in range(-l, l + 1):
+            r = int(np.searchsorted(b, abs(m), side="right") - 1)
+            out[l * (l + 1) + m] = gathered[r * lay.flm_maxlen +
+                                            int(shard.shard_flm_index(l, m, b[r], b[r + 1]))]
+    return bool(np.array_equal(out, full))
 
 
-def test_all_to_all_transposes_gloo():
-    assert all(_run(_exchange_fwd).values())
-    assert all(_run(_exchange_inv).values())
+def test_exchange_layout_all_to_all_gloo():
+    assert all(_run(_exchange_roundtrip, world=2).values())
+    assert all(_run(_exchange_roundtrip, world=3).values())
+
+
+def test_flm_blocks_all_gather_gloo():
+    assert all(_run(_flm_gather, world=2).values())
+    assert all(_run(_flm_gather, world=3).values())
+
+
+def test_flm_block_index_is_a_bijection():
+    for L, parts in [(150, 3), (97, 2), (64, 2), (33, 1)]:
+        b = shard.balanced_m_splits(L, parts) if parts > 1 else [0, L]
+        for q in range(parts):
+            m0, m1 = b[q], b[q + 1]
+            idx = [int(shard.shard_flm_index(l, m, m0, m1)) for l in range(L)
+                   for m in range(-l, l + 1) if m0 <= abs(m) < m1]
+            assert sorted(idx) == list(range(int(shard.shard_flm_base(L, m0, m1))))
 
 
 def _maps(rank, world):
