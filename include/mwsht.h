@@ -132,6 +132,17 @@ int mwsht_forward_z_batch(mwsht_plan *plan, int nmaps, const void *samples, void
 int mwsht_inverse_z_batch(mwsht_plan *plan, int nmaps, const void *flm, void *samples,
                           int spin, int recursion, void *stream);
 
+/* Multi-spin batches (the paper's footnote PAPER.md:505
+ * on transforms sharing one Wigner recursion): map b (b < nmaps <= 16, and
+ * <= max_batch) has spin spins[b] (host array).  Every (m', m) chain's
+ * recursion is spin-independent, so two maps of any spins share each chain
+ * and only their row weights Delta^l_{m',-s} and phases differ.  Same
+ * per-map results as mwsht_forward_z / mwsht_inverse_z with that spin. */
+int mwsht_forward_z_multi(mwsht_plan *plan, int nmaps, const void *samples, void *flm,
+                          const int *spins, int recursion, void *stream);
+int mwsht_inverse_z_multi(mwsht_plan *plan, int nmaps, const void *flm, void *samples,
+                          const int *spins, int recursion, void *stream);
+
 /* --------------------------------------------------- kernel-level hooks ----
  * Mirrors of torusht.kernels dispatchers (kernels/__init__.py:67-80) on
  * device buffers, for stage-by-stage parity (test_kernels.py:52-92). */

@@ -10,7 +10,8 @@ from .errors import (ContractViolationError, ConvergenceError, DeviceError,
                      InvalidBandLimitError, InvalidSpinError, SymmetryError, TorushtError,
                      UnsupportedDegreeError)
 from .mw import (HarmonicCoeffs, MwSignal, Plan, check_band_limit, clear_plans, forward,
-                 forward_batch, forward_real, get_plan, inverse, inverse_batch, inverse_real,
+                 forward_batch, forward_multi_spin, forward_real, get_plan, inverse, inverse_batch,
+                 inverse_multi_spin, inverse_real,
                  mw_grid_phis, mw_grid_thetas, reality_residual)
 from .io import load_coeffs, load_signal, read_coeffs_to, read_signal_to, save_coeffs, save_signal
 from .pipeline import HostPipeline
@@ -19,7 +20,7 @@ from .quadrature import (QuadWeights, integrate, quad_weights, quad_weights_q, r
 
 __all__ = [
     "HarmonicCoeffs", "MwSignal", "forward", "inverse", "forward_real", "inverse_real",
-    "forward_batch", "inverse_batch", "reality_residual", "HostPipeline", "check_band_limit",
+    "forward_batch", "inverse_batch", "forward_multi_spin", "inverse_multi_spin", "reality_residual", "HostPipeline", "check_band_limit",
     "mw_grid_thetas", "mw_grid_phis", "Plan", "get_plan", "clear_plans",
     "synthesize_reduced", "quad_weights", "quad_weights_q", "ring_weights_v", "weight_w",
     "integrate", "QuadWeights",

@@ -48,6 +48,8 @@ _SIGS = {
     "mwsht_reality_residual_async": ([_P, _P, _P, _P], _I),
     "mwsht_forward_z_batch": ([_P, _I, _P, _P, _I, _I, _P], _I),
     "mwsht_inverse_z_batch": ([_P, _I, _P, _P, _I, _I, _P], _I),
+    "mwsht_forward_z_multi": ([_P, _I, _P, _P, ctypes.POINTER(_I), _I, _P], _I),
+    "mwsht_inverse_z_multi": ([_P, _I, _P, _P, ctypes.POINTER(_I), _I, _P], _I),
     "mwsht_fmm_core": ([_P, _P, _P, _I, _I, _P, _P], _I),
     "mwsht_flm_core": ([_P, _P, _I, _I, _P, _P], _I),
     "mwsht_fmm_core_real": ([_P, _P, _P, _I, _P, _P], _I),

@@ -118,6 +118,12 @@ constexpr int kStages = 5;     // depth of the mbarrier ring
 
 // All 2-D plan tables and staged planes have leading dimension ldw = L rounded
 // up to kTileRows, zero-padded, so every bulk copy is in bounds and aligned.
+// Multi-spin batches: maps of different
+// spins share every chain's recursion (kap_l C_l(m') C_l(m), resp. the Trapani
+// column coefficients, do not depend on the spin); only the row weight W and
+// the phases do.  At most kMaxMsp maps per call; W-only row tables per map.
+constexpr int kMaxMsp = 16;
+
 struct InvArgs {
   DevTables t;
   const double2* rowtab;  // [l*ldw + m'] = (kap_l C_l(m'), (-1)^l lam_l u_l(m') Delta^l_{m',-s})
@@ -133,6 +139,9 @@ struct InvArgs {
   int paired;                      // tiles cover the lower triangle and also emit the transpose
   int nmaps;                       // maps in the batch (set by launch_inverse_core)
   long long g_stride, out_stride;  // per-map element strides (batch = gridDim.y)
+  int msp;                         // multi-spin: map b has spin spin_m[b], weights wrow_m[b]
+  int spin_m[kMaxMsp];
+  const double* wrow_m[kMaxMsp];   // [blk64(l, m')] = W_l(m'; spin_m[b]) (SpinTab::wrow)
 };
 
 struct FwdArgs {
@@ -146,6 +155,9 @@ struct FwdArgs {
   int nmaps;  // maps in the batch (set by launch_forward_core)
   long long in_stride, out_stride;
   int m0, m1;  // out_mode 2: the shard's order range (packed flm, shard_flm_index)
+  int msp;     // multi-spin: map b has spin spin_m[b], weights wrow_m[b]
+  int spin_m[kMaxMsp];
+  const double* wrow_m[kMaxMsp];  // [blk64(m', l)] = W'(l, m'; spin_m[b]) (SpinTab::wrowf)
 };
 
 // Packed coefficient block of an order-range shard m0 <= |m| < m1 (m-column
@@ -194,7 +206,13 @@ struct FftArgs {
   const long long* col_off;
   const int* col_stride;
   int spread;  // set by the launcher: rows dealt team-major (fft_impl.cuh first_row)
+  int msp;                // multi-spin batch: map b's spin parity is bit b of spin_par
+  unsigned long long spin_par;
 };
+// spin of map `map` as far as the FFT stages need it (its parity)
+__host__ __device__ __forceinline__ int stage_spin(const FftArgs& a, int map) {
+  return a.msp ? (int)((a.spin_par >> map) & 1ull) : a.spin;
+}
 }  // namespace fft
 
 }  // namespace mwsht

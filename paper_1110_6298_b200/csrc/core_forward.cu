@@ -34,16 +34,18 @@ namespace fwd {
 constexpr int R = kTileRows, C = kTileCols, CH = kChunk;
 // MB maps of a batch share every chain (one recursion, MB contractions);
 // their staging rows double the stage size, so the ring is one stage shorter.
-template <int MB>
+// MSP (multi-spin): each map also gets its own weights W'(l, m'; s_map).
+template <int MB, bool MSP>
 struct Stage {
   double2 q[CH][R];        // (coefficient producing y_{m'-1}, W'(l, m'))
   double2 gp[MB][CH][C];   // gfold[+m][m']
   double2 gn[MB][CH][C];   // (-1)^m' gfold[-m][m']
+  double w[MSP ? MB : 1][MSP ? CH : 1][MSP ? R : 1];  // W'(l, m'; s_map)
 };
-template <int MB>
+template <int MB, bool MSP = false>
 struct Smem {
-  static constexpr int NB = MB == 1 ? kStages : kStages - 1;
-  Stage<MB> st[NB];
+  static constexpr int NB = MSP ? kStages - 2 : (MB == 1 ? kStages : kStages - 1);
+  Stage<MB, MSP> st[NB];
   double seedy[8][kConsumerThreads];
   uint64_t full[NB], empty[NB];
 };
@@ -65,11 +67,11 @@ __device__ __forceinline__ void rescale(double (&y)[NE], double (&y1)[NE], unsig
 
 // Warp-specialised 384-thread CTA (common.cuh): warpgroup 0 = TMA producer,
 // warpgroups 1-2 = 8 consumer warps with a raised register budget.
-template <bool REAL, bool SPIN0, int MB>
+template <bool REAL, bool SPIN0, int MB, bool MSP = false>
 __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
   constexpr int NI = 4, NJ = 2, NE = NI * NJ;
   constexpr int NG = REAL ? 1 : 2;
-  using Sm = fwd::Smem<MB>;
+  using Sm = fwd::Smem<MB, MSP>;
   constexpr int NB = Sm::NB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
@@ -112,12 +114,19 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
         const int b = k % NB, mc = mu_top - k * kChunk, ns = min(kChunk, mc + 1);
         if (k >= NB) mbar_wait(&sm.empty[b], ((k / NB) - 1) & 1);
         fence_proxy_async();
-        mbar_arrive_expect_tx(&sm.full[b], ns * (fwd::R * 16u + MB * NG * fwd::C * 16u));
+        mbar_arrive_expect_tx(&sm.full[b], ns * (fwd::R * 16u + MB * NG * fwd::C * 16u +
+                                                 (MSP ? MB * fwd::R * 8u : 0u)));
         auto& S = sm.st[b];
         const int mlo = mc - ns + 1;
         const long long oc = blk<fwd::C>(mlo, c0, L);
         bulk_g2s(&S.q[fwd::CH - ns][0], a.rowtab + blk<fwd::R>(mlo, l0b, L), ns * fwd::R * 16,
                  &sm.full[b]);
+        if constexpr (MSP) {
+#pragma unroll
+          for (int mb = 0; mb < MB; mb++)
+            bulk_g2s(&S.w[mb][fwd::CH - ns][0], a.wrow_m[map_of(mb)] + blk<fwd::R>(mlo, l0b, L),
+                     ns * fwd::R * 8, &sm.full[b]);
+        }
 #pragma unroll
         for (int mb = 0; mb < MB; mb++) {
           bulk_g2s(&S.gp[mb][fwd::CH - ns][0], gpm[mb] + oc, ns * fwd::C * 16, &sm.full[b]);
@@ -198,7 +207,9 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
     const double2* rowp = &S.q[fwd::CH - 1][0] + rl0;  // step s at row CH-1-s
     const double2* gpp = &S.gp[0][fwd::CH - 1][0] + cl0;
     const double2* gnp = &S.gn[0][fwd::CH - 1][0] + cl0;
+    const double* wpp = &S.w[0][MSP ? fwd::CH - 1 : 0][0] + (MSP ? rl0 : 0);
     constexpr int MS = fwd::CH * fwd::C;  // distance between maps' staging rows
+    constexpr int MW = fwd::CH * fwd::R;  // distance between maps' weight rows (MSP)
 
     if (warp_has && wrow_hi >= mc - ns + 1) {
       if (!started) {
@@ -254,8 +265,15 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
         };
         auto full_step = [&](auto masked, int s) {
           double2 qp[NI], g[MB][NJ][NG];
+          double wv[MSP ? MB : 1][NI];
 #pragma unroll
           for (int i = 0; i < NI; i++) qp[i] = rowp[-s * fwd::R + 8 * i];
+          if constexpr (MSP) {
+#pragma unroll
+            for (int mb = 0; mb < MB; mb++)
+#pragma unroll
+              for (int i = 0; i < NI; i++) wv[mb][i] = wpp[mb * MW - s * fwd::R + 8 * i];
+          }
 #pragma unroll
           for (int mb = 0; mb < MB; mb++)
 #pragma unroll
@@ -271,12 +289,18 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
               double t = y[e] * qp[i].y;
               if (decltype(masked)::value) t = ((live >> e) & 1u) ? t : 0.0;
 #pragma unroll
-              for (int mb = 0; mb < MB; mb++)
+              for (int mb = 0; mb < MB; mb++) {
+                double tm = t;
+                if constexpr (MSP) {
+                  tm = y[e] * wv[mb][i];
+                  if (decltype(masked)::value) tm = ((live >> e) & 1u) ? tm : 0.0;
+                }
 #pragma unroll
                 for (int k2 = 0; k2 < NG; k2++) {
-                  acc[mb][e][2 * k2] = fma(t, g[mb][j][k2].x, acc[mb][e][2 * k2]);
-                  acc[mb][e][2 * k2 + 1] = fma(t, g[mb][j][k2].y, acc[mb][e][2 * k2 + 1]);
+                  acc[mb][e][2 * k2] = fma(tm, g[mb][j][k2].x, acc[mb][e][2 * k2]);
+                  acc[mb][e][2 * k2 + 1] = fma(tm, g[mb][j][k2].y, acc[mb][e][2 * k2 + 1]);
                 }
+              }
               const double yn = fma(md[j] * qp[i].x, y[e], -y1[e]);
               y1[e] = y[e];
               y[e] = yn;
@@ -342,10 +366,11 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
   }
 
   // ---------------------------------------------------------------- epilogue
-  const double sgs = (a.spin & 1) ? -1.0 : 1.0;
 #pragma unroll
   for (int mb = 0; mb < MB; mb++) {
   if (MB * (int)blockIdx.y + mb >= a.nmaps) break;
+  const int spin = MSP ? a.spin_m[map_of(mb)] : a.spin;
+  const double sgs = (spin & 1) ? -1.0 : 1.0;
   double2* __restrict__ out = a.out + (long long)map_of(mb) * a.out_stride;
 #pragma unroll
   for (int i = 0; i < NI; i++) {
@@ -359,12 +384,12 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
       const int e = i * NJ + j;
       const double2 Rp = make_double2(acc[mb][e][0], acc[mb][e][1]);
       if (a.out_mode == 2) {  // shard's packed block (m-column sharding, common.cuh)
-        const double2 f = cscale(cmul(Rp, ipow(m + a.spin)), sgs * clv);
+        const double2 f = cscale(cmul(Rp, ipow(m + spin)), sgs * clv);
         out[shard_flm_index(l, m, a.m0, a.m1)] = f;
         if (m > 0) {
           const double sl = (l & 1) ? -1.0 : 1.0;
           const double2 Rn = make_double2(sl * acc[mb][e][2], sl * acc[mb][e][3]);
-          out[shard_flm_index(l, -m, a.m0, a.m1)] = cscale(cmul(Rn, ipow(a.spin - m)), sgs * clv);
+          out[shard_flm_index(l, -m, a.m0, a.m1)] = cscale(cmul(Rn, ipow(spin - m)), sgs * clv);
         }
         continue;
       }
@@ -392,11 +417,11 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
         }
       } else {
         // (-1)^s i^(m+s) c_l R  (mw.py:317-319)
-        out[base + m] = cscale(cmul(Rp, ipow(m + a.spin)), sgs * clv);
+        out[base + m] = cscale(cmul(Rp, ipow(m + spin)), sgs * clv);
         if (m > 0) {
           const double sl = (l & 1) ? -1.0 : 1.0;
           const double2 Rn = make_double2(sl * acc[mb][e][2], sl * acc[mb][e][3]);
-          out[base - m] = cscale(cmul(Rn, ipow(a.spin - m)), sgs * clv);
+          out[base - m] = cscale(cmul(Rn, ipow(spin - m)), sgs * clv);
         }
       }
     }
@@ -404,17 +429,19 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
 }
 }
 
-template <bool REAL, bool SPIN0, int MB>
+template <bool REAL, bool SPIN0, int MB, bool MSP = false>
 static void launch_fwd(const FwdArgs& a, int ntiles, cudaStream_t st) {
-  const size_t smem = sizeof(fwd::Smem<MB>);
-  smem_attr_once((const void*)k_forward_core<REAL, SPIN0, MB>, smem);
+  const size_t smem = sizeof(fwd::Smem<MB, MSP>);
+  smem_attr_once((const void*)k_forward_core<REAL, SPIN0, MB, MSP>, smem);
   dim3 grid(ntiles, (a.nmaps + MB - 1) / MB);
-  launch_pdl(k_forward_core<REAL, SPIN0, MB>, grid, dim3(kCoreThreadsWS), smem, st, a);
+  launch_pdl(k_forward_core<REAL, SPIN0, MB, MSP>, grid, dim3(kCoreThreadsWS), smem, st, a);
 }
 
 template <int MB>
 static void launch_fwd_mb(const FwdArgs& a, int ntiles, bool real, cudaStream_t st) {
-  if (real)
+  if (a.msp)  // mixed spins: every m' contracts (no spin-0 parity skip)
+    launch_fwd<false, false, 2, true>(a, ntiles, st);
+  else if (real)
     launch_fwd<true, true, MB>(a, ntiles, st);
   else if (a.spin == 0)
     launch_fwd<false, true, MB>(a, ntiles, st);

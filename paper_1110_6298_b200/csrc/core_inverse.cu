@@ -41,17 +41,19 @@ namespace inv {
 constexpr int R = kTileRows, C = kTileCols, CH = kChunk;
 // MB maps of a batch share every chain (one recursion, MB contractions);
 // their staging rows enlarge the stage, so the ring is one stage shorter.
-template <int MB>
+// MSP (multi-spin): each map also gets its own row weights W_l(m'; s_map).
+template <int MB, bool MSP>
 struct Stage {
   double2 row[CH][R];      // (kap_l C_l(m'), W_l(m'))
   double colc[CH][C];      // C_l(m)
   double2 gp[MB][CH][C];   // c_l u_l(m) f_{l,m}
   double2 gn[MB][CH][C];   // c_l u_l(m) (-1)^l f_{l,-m}
+  double w[MSP ? MB : 1][MSP ? CH : 1][MSP ? R : 1];  // W_l(m'; s_map)
 };
-template <int MB>
+template <int MB, bool MSP = false>
 struct Smem {
-  static constexpr int NB = MB == 1 ? kStages : kStages - 1;
-  Stage<MB> st[NB];
+  static constexpr int NB = MSP ? kStages - 2 : (MB == 1 ? kStages : kStages - 1);
+  Stage<MB, MSP> st[NB];
   double seedz[8][kConsumerThreads];
   uint64_t full[NB], empty[NB];
 };
@@ -71,11 +73,11 @@ __device__ __forceinline__ void rescale(double (&z)[NE], double (&zp)[NE], unsig
   }
 }
 
-template <bool REAL, bool SPIN0, int MB>
+template <bool REAL, bool SPIN0, int MB, bool MSP = false>
 __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
   constexpr int NI = 4, NJ = 2, NE = NI * NJ;
   constexpr int NG = REAL ? 1 : 2;  // complex g values per column: f_{l,m} (+ f_{l,-m})
-  using Sm = inv::Smem<MB>;
+  using Sm = inv::Smem<MB, MSP>;
   constexpr int NB = Sm::NB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
@@ -118,10 +120,17 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
         if (k >= NB) mbar_wait(&sm.empty[b], ((k / NB) - 1) & 1);
         fence_proxy_async();
         mbar_arrive_expect_tx(&sm.full[b],
-                              ns * (inv::R * 16u + inv::C * 8u + MB * NG * inv::C * 16u));
+                              ns * (inv::R * 16u + inv::C * 8u + MB * NG * inv::C * 16u +
+                                    (MSP ? MB * inv::R * 8u : 0u)));
         auto& S = sm.st[b];
         const long long oc = blk<inv::C>(lc, c0, L);
         bulk_g2s(&S.row[0][0], rowtab + blk<inv::R>(lc, r0, L), ns * inv::R * 16, &sm.full[b]);
+        if constexpr (MSP) {
+#pragma unroll
+          for (int mb = 0; mb < MB; mb++)
+            bulk_g2s(&S.w[mb][0][0], a.wrow_m[map_of(mb)] + blk<inv::R>(lc, r0, L),
+                     ns * inv::R * 8, &sm.full[b]);
+        }
         bulk_g2s(&S.colc[0][0], a.colc + oc, ns * inv::C * 8, &sm.full[b]);
 #pragma unroll
         for (int mb = 0; mb < MB; mb++) {
@@ -206,7 +215,9 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
     const double* colp = &S.colc[0][0] + cl0;
     const double2* gpp = &S.gp[0][0][0] + cl0;
     const double2* gnp = &S.gn[0][0][0] + cl0;
+    const double* wpp = &S.w[0][0][0] + (MSP ? rl0 : 0);
     constexpr int MS = inv::CH * inv::C;  // distance between maps' staging rows
+    constexpr int MW = inv::CH * inv::R;  // distance between maps' weight rows (MSP)
 
     if (warp_has && wl0_min < lc + ns) {
       if (!started) {
@@ -270,8 +281,15 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
           double2 rp[NI];
           double cc[NJ];
           double2 g[MB][NJ][NG];
+          double wv[MSP ? MB : 1][NI];
 #pragma unroll
           for (int i = 0; i < NI; i++) rp[i] = rowp[s * inv::R + 8 * i];
+          if constexpr (MSP) {
+#pragma unroll
+            for (int mb = 0; mb < MB; mb++)
+#pragma unroll
+              for (int i = 0; i < NI; i++) wv[mb][i] = wpp[mb * MW + s * inv::R + 8 * i];
+          }
 #pragma unroll
           for (int j = 0; j < NJ; j++) {
             cc[j] = colp[s * inv::C + 8 * j];
@@ -289,12 +307,18 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
               double t = z[e] * rp[i].y;
               if (decltype(masked)::value) t = ((live >> e) & 1u) ? t : 0.0;
 #pragma unroll
-              for (int mb = 0; mb < MB; mb++)
+              for (int mb = 0; mb < MB; mb++) {
+                double tm = t;
+                if constexpr (MSP) {
+                  tm = z[e] * wv[mb][i];
+                  if (decltype(masked)::value) tm = ((live >> e) & 1u) ? tm : 0.0;
+                }
 #pragma unroll
                 for (int k2 = 0; k2 < NG; k2++) {
-                  acc[mb][e][2 * k2] = fma(t, g[mb][j][k2].x, acc[mb][e][2 * k2]);
-                  acc[mb][e][2 * k2 + 1] = fma(t, g[mb][j][k2].y, acc[mb][e][2 * k2 + 1]);
+                  acc[mb][e][2 * k2] = fma(tm, g[mb][j][k2].x, acc[mb][e][2 * k2]);
+                  acc[mb][e][2 * k2 + 1] = fma(tm, g[mb][j][k2].y, acc[mb][e][2 * k2 + 1]);
                 }
+              }
               const double zn = fma(rp[i].x * cc[j], z[e], -zp[e]);
               zp[e] = z[e];
               z[e] = zn;
@@ -359,10 +383,11 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
   }
 
   // ---------------------------------------------------------------- epilogue
-  const int sgs = (a.spin & 1) ? -1 : 1;  // (-1)^s
 #pragma unroll
   for (int mb = 0; mb < MB; mb++) {
   if (MB * (int)blockIdx.y + mb >= a.nmaps) break;
+  const int spin = MSP ? a.spin_m[map_of(mb)] : a.spin;
+  const int sgs = (spin & 1) ? -1 : 1;  // (-1)^s
   double2* __restrict__ out = a.out + (long long)map_of(mb) * a.out_stride;
 #pragma unroll
   for (int i = 0; i < NI; i++) {
@@ -399,17 +424,17 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
         if (x) row[binn] = cscale(cmul(F, twc), (m & 1) ? -1.0 : 1.0);
       } else {
         // F[m, m'] = (-1)^s i^{-(m+s)} T[m', m]; F[m, -m'] = (-1)^(m+s) F[m, m'] (mw.py:395-401)
-        const double2 Fp = cscale(cmul(Tp, ipow(-(m + a.spin))), (double)sgs);
+        const double2 Fp = cscale(cmul(Tp, ipow(-(m + spin))), (double)sgs);
         double2* rowp = out + (long long)(L - 1 + m) * N;
         rowp[binp] = cmul(Fp, tw);
-        if (x) rowp[binn] = cscale(cmul(Fp, twc), ((m + a.spin) & 1) ? -1.0 : 1.0);
+        if (x) rowp[binn] = cscale(cmul(Fp, twc), ((m + spin) & 1) ? -1.0 : 1.0);
         if (m > 0) {
           const double sx = (x & 1) ? -1.0 : 1.0;
           const double2 Tn = make_double2(sx * acc[mb][e][2], sx * acc[mb][e][3]);
-          const double2 Fn = cscale(cmul(Tn, ipow(m - a.spin)), (double)sgs);
+          const double2 Fn = cscale(cmul(Tn, ipow(m - spin)), (double)sgs);
           double2* rown = out + (long long)(L - 1 - m) * N;
           rown[binp] = cmul(Fn, tw);
-          if (x) rown[binn] = cscale(cmul(Fn, twc), ((m + a.spin) & 1) ? -1.0 : 1.0);
+          if (x) rown[binn] = cscale(cmul(Fn, twc), ((m + spin) & 1) ? -1.0 : 1.0);
         }
       }
     }
@@ -417,17 +442,19 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
 }
 }
 
-template <bool REAL, bool SPIN0, int MB>
+template <bool REAL, bool SPIN0, int MB, bool MSP = false>
 static void launch_inv(const InvArgs& a, int ntiles, cudaStream_t st) {
-  const size_t smem = sizeof(inv::Smem<MB>);
-  smem_attr_once((const void*)k_inverse_core<REAL, SPIN0, MB>, smem);
+  const size_t smem = sizeof(inv::Smem<MB, MSP>);
+  smem_attr_once((const void*)k_inverse_core<REAL, SPIN0, MB, MSP>, smem);
   dim3 grid(ntiles, (a.nmaps + MB - 1) / MB);
-  launch_pdl(k_inverse_core<REAL, SPIN0, MB>, grid, dim3(kCoreThreadsWS), smem, st, a);
+  launch_pdl(k_inverse_core<REAL, SPIN0, MB, MSP>, grid, dim3(kCoreThreadsWS), smem, st, a);
 }
 
 template <int MB>
 static void launch_inv_mb(const InvArgs& a, int ntiles, bool real, cudaStream_t st) {
-  if (real)
+  if (a.msp)  // mixed spins: every degree contracts (no spin-0 parity skip)
+    launch_inv<false, false, 2, true>(a, ntiles, st);
+  else if (real)
     launch_inv<true, true, MB>(a, ntiles, st);
   else if (a.spin == 0)
     launch_inv<false, true, MB>(a, ntiles, st);

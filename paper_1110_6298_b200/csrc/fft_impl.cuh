@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
     for (int u = 0; u < 2; u++) {
       il[u] = two ? i1 + u : i1;
       mr[u] = row_order(il[u], a.m0, a.m1, REAL);
-      eps[u] = (((mr[u] + (REAL ? 0 : a.spin)) & 1) ? -1.0 : 1.0);
+      eps[u] = (((mr[u] + (REAL ? 0 : stage_spin(a, map))) & 1) ? -1.0 : 1.0);
       g[u] = (const double2*)a.in + (long long)map * a.in_stride +
              (long long)(REAL ? mr[u] : fbin(mr[u], N)) * L;
     }
@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(kT, 1) k_theta_inv(FftArgs a) {
       sp[u] = (const double2*)a.in + (long long)map * a.in_stride + (long long)r * N;
       col[u] = REAL ? mr[u] : fbin(mr[u], N);
     }
-    const double e1 = (((mr[0] + (REAL ? 0 : a.spin)) & 1) ? -1.0 : 1.0);
+    const double e1 = (((mr[0] + (REAL ? 0 : stage_spin(a, map))) & 1) ? -1.0 : 1.0);
     double2* o = (double2*)a.out + (long long)map * a.out_stride;
     bluestein<LOGH, true>(
         X, tws, scr, a, lt, team,

@@ -26,6 +26,7 @@ void launch_inv_prescale(bool real, const double2* in, int in_mode, const double
                          int nm, cudaStream_t st, int c0 = 0, int c1 = -1);
 void launch_flm_unpack(const double2* gathered, long long maxlen, const int* bounds, int world,
                        int L, double2* flm, cudaStream_t st);
+void launch_extract_y(const double2* src, double* dst, long long n, cudaStream_t st);
 void launch_reality(const double2* f, int L, unsigned long long* red, unsigned long long* host,
                     cudaStream_t st);
 void fft_launch(int which, bool real, const fft::FftArgs& a, int nsm, cudaStream_t st);
@@ -60,6 +61,8 @@ struct SpinTab {
   double2* rowinv = nullptr;  // [blk64(l, m')] = (kap_l C_l(m'), W_l(m'))
   double2* rowfwd = nullptr;  // [blk64(m', l)] = (alpha(l-m'+1) beta(l+m'-1), W'(l, m'))
   double* wcol = nullptr;     // [blk32(l, x)] = W_l(x) (paired inverse tiles)
+  double* wrow = nullptr;     // [blk64(l, m')] = W_l(m')    (multi-spin batches, built lazily)
+  double* wrowf = nullptr;    // [blk64(m', l)] = W'(l, m')  (multi-spin batches, built lazily)
 };
 
 struct mwsht_plan {
@@ -626,6 +629,41 @@ static int check_spin(mwsht_plan* p, int spin) {
   return MWSHT_OK;
 }
 
+// W-only row tables of one spin for multi-spin batches (the cores' second
+// operand per map; the recursion coefficients come from the spin-0 tables).
+static int build_msp(mwsht_plan* p, int spin) {
+  int rc;
+  if ((rc = build_spin(p, spin))) return rc;
+  SpinTab& st = p->spins[spin];
+  if (st.wrow) return MWSHT_OK;
+  const long long n = (long long)p->L * p->ldw;
+  if ((rc = dev_alloc(p, (void**)&st.wrow, sizeof(double) * n)) ||
+      (rc = dev_alloc(p, (void**)&st.wrowf, sizeof(double) * n)))
+    return rc;
+  launch_extract_y(st.rowinv, st.wrow, n, 0);
+  launch_extract_y(st.rowfwd, st.wrowf, n, 0);
+  CU(cudaGetLastError());
+  CU(cudaDeviceSynchronize());
+  return MWSHT_OK;
+}
+
+// Validates a multi-spin batch (host spins[nm]) and builds its tables;
+// returns the spin-parity mask of the FFT stages.
+static int prepare_msp(mwsht_plan* p, int nm, const int* spins, bool real,
+                       unsigned long long* par) {
+  int rc;
+  if (real) return fail(MWSHT_E_SPIN, "multi-spin", "the real path is spin 0 only");
+  if (nm < 1 || nm > kMaxMsp || nm > p->max_batch)
+    return fail(MWSHT_E_CONTRACT, "multi-spin", "1 <= nmaps <= min(16, plan max_batch)");
+  *par = 0;
+  for (int b = 0; b < nm; b++) {
+    if ((rc = check_spin(p, spins[b]))) return rc;
+    if ((rc = build_msp(p, spins[b]))) return rc;
+    if (spins[b] & 1) *par |= 1ull << b;
+  }
+  return build_spin(p, 0);
+}
+
 // ------------------------------------------------------------ pipelines
 // Paired inverse tiles (core_inverse_paired.cu) cover the lower triangle
 // m' > m and emit the transposed outputs from the same chains.  Built for
@@ -676,10 +714,12 @@ static FwdArgs fwd_args(mwsht_plan* p, int spin) {
 // spectra AT, then the fused theta stage (k_theta_fwd: extension, DFT + twist,
 // weight correlation, m' fold: mw.py:161-285).
 static int forward_stages(mwsht_plan* p, int nm, const void* samples, bool real, int spin,
-                          cudaStream_t st) {
+                          cudaStream_t st, int msp = 0, unsigned long long spin_par = 0) {
   const int L = p->L, N = p->N;
   fft::FftArgs a = fft_args(p);
   a.spin = spin;
+  a.msp = msp;
+  a.spin_par = spin_par;
   a.nmaps = nm;
   a.nrows = L;
   a.in = samples;
@@ -698,25 +738,40 @@ static int forward_stages(mwsht_plan* p, int nm, const void* samples, bool real,
   return MWSHT_OK;
 }
 
+// spins (host, nm entries, or NULL): a multi-spin batch sharing every chain's
+// recursion between maps of different spins (kMaxMsp maps at most).
 static int do_forward(mwsht_plan* p, int nm, const void* samples, void* flm, int spin, bool real,
-                      int recursion, void* stream) {
+                      int recursion, void* stream, const int* spins = nullptr) {
   DevGuard dg;
   int rc;
   if ((rc = check_plan(p, dg))) return rc;
   if ((rc = check_rec(recursion))) return rc;
-  if ((rc = check_spin(p, spin))) return rc;
+  if (!spins && (rc = check_spin(p, spin))) return rc;
   if (real && spin != 0) return fail(MWSHT_E_SPIN, "forward_real", "spin 0 only");
   if (nm < 1 || nm > p->max_batch) return fail(MWSHT_E_CONTRACT, "nmaps", "exceeds plan max_batch");
   std::lock_guard<std::mutex> lk(p->mu);
   StreamUse su(p, (cudaStream_t)stream);
-  if ((rc = build_spin(p, spin))) return rc;
+  unsigned long long par = 0;
+  if (spins) {
+    if ((rc = prepare_msp(p, nm, spins, real, &par))) return rc;
+    spin = 0;
+  } else if ((rc = build_spin(p, spin))) {
+    return rc;
+  }
   p->own_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
   const int L = p->L;
   if (p->timing) CU(cudaEventRecord(p->ev[0][0], st));
-  if ((rc = forward_stages(p, nm, samples, real, spin, st))) return rc;
+  if ((rc = forward_stages(p, nm, samples, real, spin, st, spins ? 1 : 0, par))) return rc;
   if (p->timing) CU(cudaEventRecord(p->ev[0][1], st));
   FwdArgs a = fwd_args(p, spin);
+  if (spins) {
+    a.msp = 1;
+    for (int b = 0; b < nm; b++) {
+      a.spin_m[b] = spins[b];
+      a.wrow_m[b] = p->spins[spins[b]].wrowf;
+    }
+  }
   a.out = (double2*)flm;
   a.out_mode = 0;
   a.out_stride = (long long)L * L;
@@ -727,17 +782,23 @@ static int do_forward(mwsht_plan* p, int nm, const void* samples, void* flm, int
 }
 
 static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int spin, bool real,
-                      int recursion, void* stream) {
+                      int recursion, void* stream, const int* spins = nullptr) {
   DevGuard dg;
   int rc;
   if ((rc = check_plan(p, dg))) return rc;
   if ((rc = check_rec(recursion))) return rc;
-  if ((rc = check_spin(p, spin))) return rc;
+  if (!spins && (rc = check_spin(p, spin))) return rc;
   if (real && spin != 0) return fail(MWSHT_E_SPIN, "inverse_real", "spin 0 only");
   if (nm < 1 || nm > p->max_batch) return fail(MWSHT_E_CONTRACT, "nmaps", "exceeds plan max_batch");
   std::lock_guard<std::mutex> lk(p->mu);
   StreamUse su(p, (cudaStream_t)stream);
-  if ((rc = build_spin(p, spin))) return rc;
+  unsigned long long par = 0;
+  if (spins) {
+    if ((rc = prepare_msp(p, nm, spins, real, &par))) return rc;
+    spin = 0;
+  } else if ((rc = build_spin(p, spin))) {
+    return rc;
+  }
   p->own_launches = 0;
   cudaStream_t st = (cudaStream_t)stream;
   const int L = p->L, N = p->N;
@@ -750,6 +811,15 @@ static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int
   // 1. core + phases + m' mirror + theta twist (mw.py:378-402, 445)
   if (p->timing) CU(cudaEventRecord(p->ev[1][1], st));
   InvArgs a = inv_args(p, spin, nm);
+  if (spins) {
+    a.paired = 0;  // mixed spins share the recursion between maps instead
+    a.tiles = p->tiles_inv;
+    a.msp = 1;
+    for (int b = 0; b < nm; b++) {
+      a.spin_m[b] = spins[b];
+      a.wrow_m[b] = p->spins[spins[b]].wrow;
+    }
+  }
   a.out = p->bufB;
   a.out_mode = 0;
   a.out_stride = (long long)rows * N;
@@ -759,6 +829,8 @@ static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int
   // 2. theta synthesis (mw.py:441-446), keep t < L, transposed to rings (:436-437)
   fft::FftArgs f = fft_args(p);
   f.spin = spin;
+  f.msp = spins ? 1 : 0;
+  f.spin_par = par;
   f.nmaps = nm;
   f.nrows = rows;
   f.in = p->bufB;
@@ -924,6 +996,18 @@ int mwsht_forward_z_batch(mwsht_plan* p, int nmaps, const void* samples, void* f
 int mwsht_inverse_z_batch(mwsht_plan* p, int nmaps, const void* flm, void* samples, int spin,
                           int recursion, void* stream) {
   return do_inverse(p, nmaps, flm, samples, spin, false, recursion, stream);
+}
+
+int mwsht_forward_z_multi(mwsht_plan* p, int nmaps, const void* samples, void* flm,
+                          const int* spins, int recursion, void* stream) {
+  if (!spins) return fail(MWSHT_E_CONTRACT, "forward_z_multi", "null spins");
+  return do_forward(p, nmaps, samples, flm, 0, false, recursion, stream, spins);
+}
+
+int mwsht_inverse_z_multi(mwsht_plan* p, int nmaps, const void* flm, void* samples,
+                          const int* spins, int recursion, void* stream) {
+  if (!spins) return fail(MWSHT_E_CONTRACT, "inverse_z_multi", "null spins");
+  return do_inverse(p, nmaps, flm, samples, 0, false, recursion, stream, spins);
 }
 
 int mwsht_reality_residual(mwsht_plan* p, const void* flm, double* worst_host, double* tol_host,

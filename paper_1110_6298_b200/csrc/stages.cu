@@ -154,7 +154,20 @@ __global__ void k_flm_unpack(const double2* __restrict__ gathered, long long max
   }
 }
 
+// dst[i] = src[i].y (plan time: W-only row tables for multi-spin batches)
+__global__ void k_extract_y(const double2* __restrict__ src, double* __restrict__ dst, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i].y;
+}
+
 // ------------------------------------------------------------- launchers
+void launch_extract_y(const double2* src, double* dst, long long n, cudaStream_t st) {
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_extract_y<<<(unsigned)blocks, 256, 0, st>>>(src, dst, n);
+}
+
 void launch_flm_unpack(const double2* gathered, long long maxlen, const int* bounds, int world,
                        int L, double2* flm, cudaStream_t st) {
   long long n = (long long)L * L;

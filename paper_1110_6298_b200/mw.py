@@ -426,3 +426,69 @@ def inverse_batch(values, band_limit, spin, recursion="trapani"):
     _lib.call("mwsht_inverse_z_batch", plan.handle, B, f.data_ptr(), out.data_ptr(), spin,
               _REC_ID[recursion], _stream(dev))
     return _back(out, values)
+
+
+# ------------------------------------------------------- multi-spin batches
+
+MAX_MULTI_SPIN = 16  # maps per native call (include/mwsht.h)
+
+
+def _spins_arg(spins, B, L):
+    spins = [int(s) for s in spins]
+    if len(spins) != B:
+        raise ContractViolationError(f"need one spin per map: {B} maps, {len(spins)} spins")
+    for s in spins:
+        _check_spin(L, s)
+    return spins
+
+
+def inverse_multi_spin(values, band_limit, spins, recursion="trapani"):
+    """inverse() of B coefficient sets of different spins, (B, L^2) -> (B, L, 2L-1).
+
+    The maps share every Wigner chain's recursion, which does not depend on the
+    spin; each map contracts with its own
+    spin's row weights.  Results equal inverse() of each map with its spin.
+    """
+    L = band_limit
+    check_band_limit(L)
+    if _shape(values)[1:] != (L * L,):
+        raise ContractViolationError(f"batch coefficients must be (B, {L * L})")
+    B = _shape(values)[0]
+    spins = _spins_arg(spins, B, L)
+    for b, s in enumerate(spins):
+        if _lead_nonzero(values[b], s * s):
+            raise ContractViolationError(
+                f"map {b}: coefficients with degree below |spin|={abs(s)} must be zero")
+    _check_recursion(recursion)
+    dev = _target_device(values)
+    f = _to_device(values, torch.complex128, dev)
+    out = torch.empty((B, L, 2 * L - 1), dtype=torch.complex128, device=f"cuda:{dev}")
+    plan = get_plan(L, dev, max_batch=min(B, MAX_MULTI_SPIN))
+    for b0 in range(0, B, MAX_MULTI_SPIN):
+        nb = min(MAX_MULTI_SPIN, B - b0)
+        arr = (_lib.ctypes.c_int * nb)(*spins[b0:b0 + nb])
+        _lib.call("mwsht_inverse_z_multi", plan.handle, nb, f[b0].data_ptr(), out[b0].data_ptr(),
+                  arr, _REC_ID[recursion], _stream(dev))
+    return _back(out, values)
+
+
+def forward_multi_spin(samples, band_limit, spins, recursion="trapani"):
+    """forward() of B maps of different spins, (B, L, 2L-1) -> (B, L^2), sharing
+    the recursion like inverse_multi_spin."""
+    L = band_limit
+    check_band_limit(L)
+    if _shape(samples)[1:] != (L, 2 * L - 1):
+        raise ContractViolationError(f"batch samples must be (B, {L}, {2 * L - 1})")
+    B = _shape(samples)[0]
+    spins = _spins_arg(spins, B, L)
+    _check_recursion(recursion)
+    dev = _target_device(samples)
+    x = _to_device(samples, torch.complex128, dev)
+    out = torch.empty((B, L * L), dtype=torch.complex128, device=f"cuda:{dev}")
+    plan = get_plan(L, dev, max_batch=min(B, MAX_MULTI_SPIN))
+    for b0 in range(0, B, MAX_MULTI_SPIN):
+        nb = min(MAX_MULTI_SPIN, B - b0)
+        arr = (_lib.ctypes.c_int * nb)(*spins[b0:b0 + nb])
+        _lib.call("mwsht_forward_z_multi", plan.handle, nb, x[b0].data_ptr(), out[b0].data_ptr(),
+                  arr, _REC_ID[recursion], _stream(dev))
+    return _back(out, samples)
