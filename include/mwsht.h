@@ -217,6 +217,24 @@ int mwsht_shard_inverse_phi(mwsht_plan *plan, const void *in, int t0, int t1,
 int mwsht_shard_unpack_flm(mwsht_plan *plan, const void *gathered, long long maxlen,
                            const int *bounds, int world, void *flm, void *stream);
 
+/* ------------------------------------------------ Gauss-Legendre comparator ----
+ * gl_fm_core(flm_scaled, x, ch, sh, L, spin) -> F     (_numba.py:237-268)
+ * gl_flm_core(a, x, ch, sh, L, spin) -> R             (_numba.py:211-234)
+ * Device arrays: flm_scaled (L, N) and R (L, N) complex; a and F (N, L)
+ * complex (row = order m + L - 1, column = node); x, ch, sh (L,) float64 (nodes,
+ * cos(theta/2), sin(theta/2)); per order row mi the seed of _seed_d
+ * (_numba.py:191-208): seed_const[mi] = sign sqrt(C(2nn, nn+mm)) and
+ * seed_ints[4 mi .. 4 mi + 2] = (ec, es, l0) (the host binding computes them
+ * with the reference's lgamma/exp formula).  No plan: stateless kernels on the
+ * current device; L <= 4096 (the stability gate L <= 1024 is the host
+ * binding's, gl.py:98-104). */
+int mwsht_gl_fm_core(const void *flm_scaled, const double *x, const double *ch, const double *sh,
+                     const double *seed_const, const int *seed_ints, int L, int spin, void *F,
+                     void *stream);
+int mwsht_gl_flm_core(const void *a, const double *x, const double *ch, const double *sh,
+                      const double *seed_const, const int *seed_ints, int L, int spin, void *R,
+                      void *stream);
+
 /* Inverse-core tiling (no reference counterpart; a scheduling choice only).
  * Paired tiles: each (m', m) chain with m' > m also produces the transposed
  * output T[m, m'] (Delta^l_{m m'} = (-1)^(m'-m) Delta^l_{m' m}), so one

@@ -431,3 +431,135 @@ def gaussian_real_coeffs(L, seed):
             v[base + m] = pos
             v[base - m] = np.where(m % 2 == 0, 1.0, -1.0) * np.conj(pos)
     return v
+
+
+# ------------------------------------------------ Gauss-Legendre comparator
+# Restatement of the reference's gl_flm_core / gl_fm_core (_numba.py:191-268),
+# vectorised over the order rows mi with the reference's per-element operation
+# order (every (l, mi) sum runs over the nodes i in increasing i, as there).
+
+def _libm():
+    """The C math library's lgamma/exp: the reference's numba _seed_d
+    (_numba.py:191-208) calls these, not CPython's own math.lgamma."""
+    import ctypes
+    import ctypes.util
+    lib = ctypes.CDLL(ctypes.util.find_library("m") or "libm.so.6")
+    for name in ("lgamma", "exp"):
+        getattr(lib, name).restype = ctypes.c_double
+        getattr(lib, name).argtypes = [ctypes.c_double]
+    return lib
+
+
+_LIBM = _libm()
+
+
+def _gl_seeds(L, spin):
+    n = -spin
+    N = 2 * L - 1
+    cst, ec, es, l0 = np.zeros(N), np.zeros(N), np.zeros(N), np.zeros(N, dtype=np.int64)
+    for mi in range(N):
+        m = mi - (L - 1)
+        if n >= abs(m):
+            mm, nn, sign = m, n, 1.0
+        elif n <= -abs(m):
+            mm, nn, sign = -m, -n, (-1.0 if (m - n) % 2 else 1.0)
+        elif m >= abs(n):
+            mm, nn, sign = n, m, (-1.0 if (m - n) % 2 else 1.0)
+        else:
+            mm, nn, sign = -n, -m, 1.0
+        cst[mi] = sign * _LIBM.exp(0.5 * (_LIBM.lgamma(2 * nn + 1.0) - _LIBM.lgamma(nn + mm + 1.0)
+                                          - _LIBM.lgamma(nn - mm + 1.0)))
+        ec[mi], es[mi], l0[mi] = nn + mm, nn - mm, nn
+    return cst, ec, es, l0
+
+
+def _int_power(a, e):
+    """float ** int as numba evaluates it (exponentiation by squaring from
+    r = 1, the reference's ch[i] ** ec with integer ec)."""
+    e = np.asarray(e, dtype=np.int64).copy()
+    r = np.ones(e.shape)
+    base = np.full(e.shape, float(a))
+    while np.any(e != 0):
+        odd = (e & 1) == 1
+        r = np.where(odd, r * base, r)
+        e >>= 1
+        base = base * base
+    return r
+
+
+def _gl_chains(L, spin, x, ch, sh, visit):
+    """Run every (mi, node) chain; visit(el, i, dl, active) per degree."""
+    n = -spin
+    N = 2 * L - 1
+    m = np.arange(N) - (L - 1)
+    cst, ec, es, l0 = _gl_seeds(L, spin)
+    mf = m.astype(np.float64)
+    for i in range(L):
+        xi = x[i]
+        dl = np.zeros(N)
+        dlm1 = np.zeros(N)
+        for el in range(L):
+            start = l0 == el
+            if np.any(start):
+                dl[start] = cst[start] * _int_power(ch[i], ec[start]) * _int_power(sh[i], es[start])
+                dlm1[start] = 0.0
+            active = l0 <= el
+            visit(el, i, dl, active)
+            if el == L - 1:
+                break
+            if el == 0:
+                nxt = xi * dl
+            else:
+                with np.errstate(invalid="ignore"):
+                    den = el * np.sqrt(((el + 1.0) ** 2 - mf * mf) * ((el + 1.0) ** 2 - n * n))
+                    t = ((2.0 * el + 1.0) * (el * (el + 1.0) * xi - m * n) * dl
+                         - (el + 1.0) * np.sqrt((el * el - mf * mf) * (el * el - n * n)) * dlm1)
+                    nxt = t / den
+            dlm1 = np.where(active, dl, dlm1)
+            dl = np.where(active, nxt, dl)
+
+
+def gl_flm_core(a, x, ch, sh, L, spin):
+    R = np.zeros((L, 2 * L - 1), dtype=np.complex128)
+
+    def visit(el, i, dl, active):
+        R[el, active] += dl[active] * a[active, i]
+
+    _gl_chains(L, spin, x, ch, sh, visit)
+    return R
+
+
+def gl_fm_core(flm_scaled, x, ch, sh, L, spin):
+    F = np.zeros((2 * L - 1, L), dtype=np.complex128)
+    acc = {}
+
+    def visit(el, i, dl, active):
+        if el == 0:
+            acc[i] = np.zeros(2 * L - 1, dtype=np.complex128)
+        acc[i][active] += flm_scaled[el, active] * dl[active]
+        if el == L - 1:
+            F[:, i] = acc.pop(i)
+
+    _gl_chains(L, spin, x, ch, sh, visit)
+    return F
+
+
+def gl_forward(samples, L, spin, nodes, weights):
+    """gl.py:114-148 with the oracle's core."""
+    gm = np.fft.fftshift(np.fft.fft(samples, axis=1), axes=1) * (2.0 * math.pi / (2 * L - 1))
+    a = np.ascontiguousarray(gm.T * weights[None, :])
+    ch, sh = np.sqrt((1.0 + nodes) / 2.0), np.sqrt((1.0 - nodes) / 2.0)
+    out2d = gl_flm_core(a, nodes, ch, sh, L, spin) * cl_table(L)[:, None]
+    if spin % 2:
+        out2d = -out2d
+    return to_flat(out2d, L)
+
+
+def gl_inverse(values, L, spin, nodes):
+    """gl.py:151-178 with the oracle's core."""
+    flm_scaled = from_flat(values, L) * cl_table(L)[:, None]
+    if spin % 2:
+        flm_scaled = -flm_scaled
+    ch, sh = np.sqrt((1.0 + nodes) / 2.0), np.sqrt((1.0 - nodes) / 2.0)
+    F = gl_fm_core(flm_scaled, nodes, ch, sh, L, spin)
+    return np.fft.ifft(np.fft.ifftshift(F.T, axes=1), axis=1) * (2 * L - 1)

@@ -13,6 +13,7 @@ from .mw import (HarmonicCoeffs, MwSignal, Plan, check_band_limit, clear_plans, 
                  forward_batch, forward_multi_spin, forward_real, get_plan, inverse, inverse_batch,
                  inverse_multi_spin, inverse_real,
                  mw_grid_phis, mw_grid_thetas, reality_residual)
+from .gl import GlGrid, STABLE_BAND_LIMIT, gl_forward, gl_inverse, gl_nodes
 from .io import load_coeffs, load_signal, read_coeffs_to, read_signal_to, save_coeffs, save_signal
 from .pipeline import HostPipeline
 from .quadrature import (QuadWeights, integrate, quad_weights, quad_weights_q, ring_weights_v,
@@ -23,7 +24,8 @@ __all__ = [
     "forward_batch", "inverse_batch", "forward_multi_spin", "inverse_multi_spin", "reality_residual", "HostPipeline", "check_band_limit",
     "mw_grid_thetas", "mw_grid_phis", "Plan", "get_plan", "clear_plans",
     "synthesize_reduced", "quad_weights", "quad_weights_q", "ring_weights_v", "weight_w",
-    "integrate", "QuadWeights",
+    "integrate", "QuadWeights", "GlGrid", "gl_nodes", "gl_forward", "gl_inverse",
+    "STABLE_BAND_LIMIT",
     "save_coeffs", "load_coeffs", "save_signal", "load_signal", "read_coeffs_to", "read_signal_to",
     "TorushtError", "InvalidBandLimitError", "InvalidSpinError", "ContractViolationError",
     "UnsupportedDegreeError", "SymmetryError", "ConvergenceError", "DeviceError",

@@ -50,6 +50,8 @@ _SIGS = {
     "mwsht_inverse_z_batch": ([_P, _I, _P, _P, _I, _I, _P], _I),
     "mwsht_forward_z_multi": ([_P, _I, _P, _P, ctypes.POINTER(_I), _I, _P], _I),
     "mwsht_inverse_z_multi": ([_P, _I, _P, _P, ctypes.POINTER(_I), _I, _P], _I),
+    "mwsht_gl_fm_core": ([_P, _P, _P, _P, _P, _P, _I, _I, _P, _P], _I),
+    "mwsht_gl_flm_core": ([_P, _P, _P, _P, _P, _P, _I, _I, _P, _P], _I),
     "mwsht_fmm_core": ([_P, _P, _P, _I, _I, _P, _P], _I),
     "mwsht_flm_core": ([_P, _P, _I, _I, _P, _P], _I),
     "mwsht_fmm_core_real": ([_P, _P, _P, _I, _P, _P], _I),

@@ -27,6 +27,9 @@ void launch_inv_prescale(bool real, const double2* in, int in_mode, const double
 void launch_flm_unpack(const double2* gathered, long long maxlen, const int* bounds, int world,
                        int L, double2* flm, cudaStream_t st);
 void launch_extract_y(const double2* src, double* dst, long long n, cudaStream_t st);
+cudaError_t launch_gl(bool forward, const double2* in, const double* x, const double* ch,
+              const double* sh, const double* cst, const int4* seed, int L, int spin,
+              double2* out, cudaStream_t st);
 void launch_reality(const double2* f, int L, unsigned long long* red, unsigned long long* host,
                     cudaStream_t st);
 void fft_launch(int which, bool real, const fft::FftArgs& a, int nsm, cudaStream_t st);
@@ -1294,6 +1297,33 @@ int mwsht_shard_unpack_flm(mwsht_plan* p, const void* gathered, long long maxlen
                     (cudaStream_t)stream);
   LAUNCHED(p);
   return MWSHT_OK;
+}
+
+static int gl_core(bool forward, const void* in, const double* x, const double* ch,
+                   const double* sh, const double* seed_const, const int* seed_ints, int L,
+                   int spin, void* out, void* stream) {
+  if (L < 1) return fail(MWSHT_E_BAND_LIMIT, "gl", "band limit must be >= 1");
+  if ((spin < 0 ? -spin : spin) >= L) return fail(MWSHT_E_SPIN, "gl", "|spin| must be below L");
+  if (L > 4096) return fail(MWSHT_E_DEGREE, "gl", "band limit above the kernels' cap L <= 4096");
+  if (!in || !x || !ch || !sh || !seed_const || !seed_ints || !out)
+    return fail(MWSHT_E_CONTRACT, "gl", "null buffer");
+  const cudaError_t e = launch_gl(forward, (const double2*)in, x, ch, sh, seed_const,
+                                  (const int4*)seed_ints, L, spin, (double2*)out,
+                                  (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(MWSHT_E_CUDA, "gl kernel launch", cudaGetErrorString(e));
+  return MWSHT_OK;
+}
+
+int mwsht_gl_fm_core(const void* flm_scaled, const double* x, const double* ch, const double* sh,
+                     const double* seed_const, const int* seed_ints, int L, int spin, void* F,
+                     void* stream) {
+  return gl_core(false, flm_scaled, x, ch, sh, seed_const, seed_ints, L, spin, F, stream);
+}
+
+int mwsht_gl_flm_core(const void* a, const double* x, const double* ch, const double* sh,
+                      const double* seed_const, const int* seed_ints, int L, int spin, void* R,
+                      void* stream) {
+  return gl_core(true, a, x, ch, sh, seed_const, seed_ints, L, spin, R, stream);
 }
 
 int mwsht_plan_set_paired(mwsht_plan* p, int mode) {

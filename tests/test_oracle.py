@@ -109,3 +109,30 @@ def test_oracle_reduced_grid_and_quadrature_match_reference(L, s):
     q = O.quad_weights_q(L, s)
     assert np.max(np.abs(q - g[key + "_q"])) == 0.0
     assert O.integrate(g[key + "_reduced"], q) == complex(g[key + "_integral"])
+
+
+def test_gl_oracle_matches_reference_golden():
+    # oracle/'s restatement of gl_flm_core / gl_fm_core (_numba.py:191-268)
+    # against the reference's own gl_inverse / gl_forward outputs
+    import os
+    import numpy as np
+    from helpers import random_signal
+    from oracle import mw_oracle as O
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "gl.npz"))
+    for L, s in [(1, 0), (2, 0), (2, 1), (8, 0), (8, -3), (33, 2), (64, -1)]:
+        k = f"L{L}_s{s}"
+        inv = O.gl_inverse(O.gaussian_coeffs(L, s, 100 + L), L, s, g[k + "_nodes"])
+        fwd = O.gl_forward(random_signal(L, s, 200 + L), L, s, g[k + "_nodes"], g[k + "_weights"])
+        assert np.array_equal(inv, g[k + "_inverse"]), k
+        assert np.array_equal(fwd, g[k + "_forward"]), k
+
+
+def test_gl_nodes_match_reference_golden():
+    import os
+    import numpy as np
+    from paper_1110_6298_b200.gl import gl_nodes
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "gl.npz"))
+    for L, s in [(1, 0), (2, 0), (8, 0), (33, 2), (64, -1), (128, 0)]:
+        grid = gl_nodes(L)
+        assert np.array_equal(grid.nodes, g[f"L{L}_s{s}_nodes"])
+        assert np.array_equal(grid.weights, g[f"L{L}_s{s}_weights"])
