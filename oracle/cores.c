@@ -86,24 +86,46 @@ static void share(int n, int tid, int nt, int *lo, int *hi) {
 
 /* ------------------------------------------------------------ recursions */
 
-/* _numba.py:18-41, rows [i0, i1) of the half step */
+/* _numba.py:18-41, rows [i0, i1) of the half step.  Every entry is computed
+ * with the reference's expression and operation order (acc = 0.0, then
+ * acc += ri*rk*cc*src[..] etc., dst = acc / two_j); the branches on i and k
+ * are only hoisted out of the inner loop (boundary rows/columns peeled), so
+ * the interior loop vectorises without changing any entry's bits. */
 static void risbo_half_rows(const double *src, int ld, double *dst, int two_j, double cc,
                             double ss, const double *rt, int i0, int i1) {
-  int n1 = two_j + 1;
+  const double dj = (double)two_j;
   for (int i = i0; i < i1; i++) {
-    double ri = rt[i], ui = rt[two_j - i];
-    for (int k = 0; k < n1; k++) {
-      double rk = rt[k], uk = rt[two_j - k];
+    const double ri = rt[i], ui = rt[two_j - i];
+    const double *sp = i > 0 ? src + (long)(i - 1) * ld : NULL;  /* row i-1 */
+    const double *sc = i < two_j ? src + (long)i * ld : NULL;    /* row i   */
+    double *d = dst + (long)i * ld;
+    for (int k = 0; k <= two_j; k++) {
+      if (k == 1 && sp && sc && two_j >= 2) {
+        /* interior columns 1 <= k < two_j, all four terms */
+        const int kend = two_j;
+        for (int kk = 1; kk < kend; kk++) {
+          const double rk = rt[kk], uk = rt[two_j - kk];
+          double acc = 0.0;
+          acc += ri * rk * cc * sp[kk - 1];
+          acc -= ri * uk * ss * sp[kk];
+          acc += ui * rk * ss * sc[kk - 1];
+          acc += ui * uk * cc * sc[kk];
+          d[kk] = acc / dj;
+        }
+        k = kend - 1;
+        continue;
+      }
+      const double rk = rt[k], uk = rt[two_j - k];
       double acc = 0.0;
-      if (i > 0) {
-        if (k > 0) acc += ri * rk * cc * src[(i - 1) * ld + (k - 1)];
-        if (k < two_j) acc -= ri * uk * ss * src[(i - 1) * ld + k];
+      if (sp) {
+        if (k > 0) acc += ri * rk * cc * sp[k - 1];
+        if (k < two_j) acc -= ri * uk * ss * sp[k];
       }
-      if (i < two_j) {
-        if (k > 0) acc += ui * rk * ss * src[i * ld + (k - 1)];
-        if (k < two_j) acc += ui * uk * cc * src[i * ld + k];
+      if (sc) {
+        if (k > 0) acc += ui * rk * ss * sc[k - 1];
+        if (k < two_j) acc += ui * uk * cc * sc[k];
       }
-      dst[i * ld + k] = acc / two_j;
+      d[k] = acc / two_j;
     }
   }
 }
