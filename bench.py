@@ -205,7 +205,7 @@ def cpu_full_pair(wl, threads):
     return time.perf_counter() - t0
 
 
-def cpu_prefix_estimate(wl, threads, budget_s):
+def cpu_prefix_estimate(wl, threads, budget_s, lp_fixed=None):
     """Seconds per pair estimated from the FFT stages at full L plus the
     cores on a degree prefix l < L' scaled by (L/L')^3 (bounded sample)."""
     from oracle import mw_oracle as O
@@ -223,7 +223,7 @@ def cpu_prefix_estimate(wl, threads, budget_s):
     if wl["real"]:
         t_fft *= 0.5
     remaining = max(2.0, budget_s - t_fft)
-    Lp = 128
+    Lp = lp_fixed or 128
     while True:
         v = O.gaussian_coeffs(Lp, spin, 0)
         flm2d = O.from_flat(v, Lp)
@@ -234,7 +234,7 @@ def cpu_prefix_estimate(wl, threads, budget_s):
         t_core = time.perf_counter() - t0
         if wl["real"]:
             t_core *= 0.5
-        if t_core * 8 > remaining or Lp * 2 > L:
+        if lp_fixed or t_core * 8 > remaining or Lp * 2 > L:
             break
         Lp *= 2
     scale = (L / Lp) ** 3
@@ -289,7 +289,8 @@ def run_reference(args, wl, ws):
     # range, so the serial figure is a full measurement.
     serial_pp, serial_desc, t_fft, core_1 = cpu_prefix_estimate(wl, 1, budget_s=20.0)
     if L > 1024:
-        _, _, _, core_n = cpu_prefix_estimate(wl, threads, budget_s=20.0)
+        lp = int(serial_desc.split("prefix l<")[1].split(" ")[0])
+        _, _, _, core_n = cpu_prefix_estimate(wl, threads, budget_s=20.0, lp_fixed=lp)
         speedup = max(1.0, core_1 / max(1e-9, core_n))
         serial_pp = t_fft + (t_pair - t_fft) * speedup
         serial_desc = (f"estimated: the measured full pair's core time x the {threads}-thread "
