@@ -19,6 +19,10 @@
 namespace mwsht {
 void launch_inverse_core(const InvArgs& a, int ntiles, int nmaps, bool real, cudaStream_t st);
 void launch_forward_core(const FwdArgs& a, int ntiles, int nmaps, bool real, cudaStream_t st);
+int small_inverse_limit();
+int small_forward_limit();
+void launch_inverse_small(const InvArgs& a, int nmaps, bool real, cudaStream_t st);
+void launch_forward_small(const FwdArgs& a, int nmaps, bool real, cudaStream_t st);
 void launch_fold(bool real, const double2* gf, double2* gfT, int L, int ldw, cudaStream_t st);
 void launch_T2_to_fold(bool real, const double2* gfT, double2* gf, int L, int ldw, cudaStream_t st);
 void launch_inv_prescale(bool real, const double2* in, int in_mode, const double* cl,
@@ -667,6 +671,28 @@ static int prepare_msp(mwsht_plan* p, int nm, const int* spins, bool real,
   return build_spin(p, 0);
 }
 
+// Core launch for a whole (unsharded) transform: small band limits run the
+// one-thread-per-chain cores (core_small.cu), the rest the tiled cores.
+static void core_inverse(const mwsht_plan* p, InvArgs a, int ntiles, int nm, bool real,
+                         cudaStream_t st) {
+  if (!a.msp && a.out_mode != 2 && p->L <= small_inverse_limit()) {
+    a.nmaps = nm;
+    launch_inverse_small(a, nm, real, st);
+  } else {
+    launch_inverse_core(a, ntiles, nm, real, st);
+  }
+}
+
+static void core_forward(const mwsht_plan* p, FwdArgs a, int ntiles, int nm, bool real,
+                         cudaStream_t st) {
+  if (!a.msp && a.out_mode != 2 && p->L <= small_forward_limit()) {
+    a.nmaps = nm;
+    launch_forward_small(a, nm, real, st);
+  } else {
+    launch_forward_core(a, ntiles, nm, real, st);
+  }
+}
+
 // ------------------------------------------------------------ pipelines
 // Paired inverse tiles (core_inverse_paired.cu) cover the lower triangle
 // m' > m and emit the transposed outputs from the same chains.  Built for
@@ -778,7 +804,7 @@ static int do_forward(mwsht_plan* p, int nm, const void* samples, void* flm, int
   a.out = (double2*)flm;
   a.out_mode = 0;
   a.out_stride = (long long)L * L;
-  launch_forward_core(a, p->ntiles_fwd, nm, real, st);
+  core_forward(p, a, p->ntiles_fwd, nm, real, st);
   LAUNCHED(p);
   if (p->timing) CU(cudaEventRecord(p->ev[0][2], st));
   return MWSHT_OK;
@@ -826,7 +852,7 @@ static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int
   a.out = p->bufB;
   a.out_mode = 0;
   a.out_stride = (long long)rows * N;
-  launch_inverse_core(a, inv_ntiles(p, a), nm, real, st);
+  core_inverse(p, a, inv_ntiles(p, a), nm, real, st);
   LAUNCHED(p);
   if (p->timing) CU(cudaEventRecord(p->ev[1][2], st));
   // 2. theta synthesis (mw.py:441-446), keep t < L, transposed to rings (:436-437)
@@ -1063,7 +1089,7 @@ int mwsht_fmm_core(mwsht_plan* p, const void* flm2d, const double* cl, int spin,
   InvArgs a = inv_args(p, spin);
   a.out = (double2*)T;
   a.out_mode = 1;
-  launch_inverse_core(a, inv_ntiles(p, a), 1, false, st);
+  core_inverse(p, a, inv_ntiles(p, a), 1, false, st);
   LAUNCHED(p);
   return MWSHT_OK;
 }
@@ -1084,7 +1110,7 @@ int mwsht_fmm_core_real(mwsht_plan* p, const void* flm_half, const double* cl, i
   InvArgs a = inv_args(p, 0);
   a.out = (double2*)T;
   a.out_mode = 1;
-  launch_inverse_core(a, inv_ntiles(p, a), 1, true, st);
+  core_inverse(p, a, inv_ntiles(p, a), 1, true, st);
   LAUNCHED(p);
   return MWSHT_OK;
 }
@@ -1107,7 +1133,7 @@ int mwsht_flm_core(mwsht_plan* p, const void* gfold, int spin, int use_trapani, 
   a.out_mode = 1;
   // entries |m| > l stay zero, as in the reference's np.zeros output
   CU(cudaMemsetAsync(R, 0, sizeof(double2) * (size_t)p->L * p->N, st));
-  launch_forward_core(a, p->ntiles_fwd, 1, false, st);
+  core_forward(p, a, p->ntiles_fwd, 1, false, st);
   LAUNCHED(p);
   return MWSHT_OK;
 }
@@ -1127,7 +1153,7 @@ int mwsht_flm_core_real(mwsht_plan* p, const void* gfold, int use_trapani, void*
   a.out = (double2*)R;
   a.out_mode = 1;
   CU(cudaMemsetAsync(R, 0, sizeof(double2) * (size_t)p->L * p->L, st));
-  launch_forward_core(a, p->ntiles_fwd, 1, true, st);
+  core_forward(p, a, p->ntiles_fwd, 1, true, st);
   LAUNCHED(p);
   return MWSHT_OK;
 }
