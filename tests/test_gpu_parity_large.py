@@ -131,3 +131,25 @@ def test_golden_C5_L4096_oracle_risbo(mw, O, spin):
     raw = torch.from_numpy(random_signal(L, spin, int(g["raw_seed"]))).cuda()
     flm = mw.forward(mw.MwSignal(L, spin, raw), recursion="risbo").values
     _check_fwd(O, g, flm.cpu().numpy(), L, 2e-12)
+
+
+@pytest.mark.parametrize("L,spin,real", [(64, 0, False), (256, -2, False), (1024, 0, True),
+                                         (1024, 2, False)])
+def test_config_full_arrays_match_oracle(mw, O, L, spin, real):
+    # C1-C3 (and C3's size at spin 2) compared on the WHOLE arrays, not a
+    # subsample: the inverse of the seeded BASELINE coefficients and the forward
+    # of those samples, against the oracle (the reference's algorithm)
+    if real:
+        v = O.gaussian_real_coeffs(L, 0)
+        sig = mw.inverse_real(mw.HarmonicCoeffs(L, 0, v.copy())).samples
+        ref = O.inverse_real(v, L, threads=THREADS)
+        back = mw.forward_real(mw.MwSignal(L, 0, np.array(sig))).values
+        ref_back = O.forward_real(ref, L, threads=THREADS)
+    else:
+        v = O.gaussian_coeffs(L, spin, 0)
+        sig = mw.inverse(mw.HarmonicCoeffs(L, spin, v.copy())).samples
+        ref = O.inverse(v, L, spin, threads=THREADS)
+        back = mw.forward(mw.MwSignal(L, spin, np.array(sig))).values
+        ref_back = O.forward(ref, L, spin, threads=THREADS)
+    assert rel(sig, ref) < 1e-12
+    assert rel(back, ref_back) < 1e-12
