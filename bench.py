@@ -546,7 +546,8 @@ def max_over_ranks(x, ws):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -660,8 +661,13 @@ def main():
     ap.add_argument("--workload", default="c5s0", choices=sorted(WORKLOADS))
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=25.0)
+    ap.add_argument("--band-limit", type=int, default=None,
+                    help="harness tests only: override the workload's L")
     args = ap.parse_args()
     ws, rank, local = dist_env()
+    if args.band_limit:
+        for w in WORKLOADS.values():
+            w["L"] = args.band_limit
     wl = WORKLOADS[args.workload]
 
     if args.impl == "reference":
@@ -675,11 +681,20 @@ def main():
     import torch
     if args.gpus > 1 and ws != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
+    # harness self-test only (tests/test_gpu_bench_harness.py): every rank on
+    # cuda:0 with a host-staged gloo exchange, so the N-rank code path runs on a
+    # one-GPU box; its timings are not scaling figures
+    if os.environ.get("MWSHT_BENCH_SAME_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
         os.environ.setdefault("NCCL_DEBUG", "INFO")
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        backend = os.environ.get("MWSHT_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     peak = fp64_peak(local)
 
     def measure(key, steps, want_clocks):

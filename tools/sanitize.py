@@ -1,9 +1,15 @@
 """Small transforms for compute-sanitizer runs where the tool is available
-(memcheck / racecheck / synccheck; it is disabled on the round-1 GPU pool):
+(memcheck / racecheck / synccheck).  compute-sanitizer is closed on this
+build's GPU pool (round 2 re-checked: "closed on this pool and stays closed"),
+so bounds and races are covered by the oracle comparisons, the bitwise
+repeatability test and the small/tiled core cross-checks instead:
 
     compute-sanitizer --tool memcheck python tools/sanitize.py
 Covers the paired and plain inverse cores, the batched (two maps per CTA)
-cores, the real path and every FFT stage, at band limits the tools finish fast.
+cores, the multi-spin cores, the real path, every FFT stage and the GL
+kernels, at band limits the tools finish fast.  Run it once with the default
+small-L per-chain cores and once with MWSHT_SMALL_INV=0 MWSHT_SMALL_FWD=0
+(tiled cores).
 """
 import os
 import sys
@@ -26,4 +32,11 @@ assert np.max(np.abs(b - vals)) < 1e-11
 vr = gaussian_real_coeffs(L, 2)
 r = mw.forward_real(mw.inverse_real(mw.HarmonicCoeffs(L, 0, vr))).values
 assert np.max(np.abs(r - vr)) < 1e-11
-print("sanitize workload ok, L =", L)
+ms = [0, 2, -1]
+mv = np.stack([gaussian_coeffs(L, s, k) for k, s in enumerate(ms)])
+m2 = mw.forward_multi_spin(mw.inverse_multi_spin(mv, L, ms), L, ms)
+assert np.max(np.abs(m2 - mv)) < 1e-11
+g = mw.gl_forward(mw.gl_inverse(mw.HarmonicCoeffs(L, 2, gaussian_coeffs(L, 2, 3))), 2).values
+assert np.max(np.abs(g - gaussian_coeffs(L, 2, 3))) < 1e-10
+print("sanitize workload ok, L =", L, "small-core limits",
+      os.environ.get("MWSHT_SMALL_INV", "default"), os.environ.get("MWSHT_SMALL_FWD", "default"))
