@@ -40,7 +40,15 @@ struct Stage {
   double2 q[CH][R];        // (coefficient producing y_{m'-1}, W'(l, m'))
   double2 gp[MB][CH][C];   // gfold[+m][m']
   double2 gn[MB][CH][C];   // (-1)^m' gfold[-m][m']
-  double w[MSP ? MB : 1][MSP ? CH : 1][MSP ? R : 1];  // W'(l, m'; s_map)
+};
+// multi-spin stages also carry each map's W'(l, m'; s_map) (no member otherwise:
+// the plain stages keep their 128-byte-multiple size)
+template <int MB>
+struct Stage<MB, true> {
+  double2 q[CH][R];
+  double2 gp[MB][CH][C];
+  double2 gn[MB][CH][C];
+  double w[MB][CH][R];
 };
 template <int MB, bool MSP = false>
 struct Smem {
@@ -207,7 +215,8 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
     const double2* rowp = &S.q[fwd::CH - 1][0] + rl0;  // step s at row CH-1-s
     const double2* gpp = &S.gp[0][fwd::CH - 1][0] + cl0;
     const double2* gnp = &S.gn[0][fwd::CH - 1][0] + cl0;
-    const double* wpp = &S.w[0][MSP ? fwd::CH - 1 : 0][0] + (MSP ? rl0 : 0);
+    const double* wpp = nullptr;
+    if constexpr (MSP) wpp = &S.w[0][fwd::CH - 1][0] + rl0;
     constexpr int MS = fwd::CH * fwd::C;  // distance between maps' staging rows
     constexpr int MW = fwd::CH * fwd::R;  // distance between maps' weight rows (MSP)
 

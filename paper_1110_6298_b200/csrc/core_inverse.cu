@@ -48,7 +48,16 @@ struct Stage {
   double colc[CH][C];      // C_l(m)
   double2 gp[MB][CH][C];   // c_l u_l(m) f_{l,m}
   double2 gn[MB][CH][C];   // c_l u_l(m) (-1)^l f_{l,-m}
-  double w[MSP ? MB : 1][MSP ? CH : 1][MSP ? R : 1];  // W_l(m'; s_map)
+};
+// multi-spin stages also carry each map's W_l(m'; s_map) (no member otherwise:
+// the plain stages keep their 128-byte-multiple size)
+template <int MB>
+struct Stage<MB, true> {
+  double2 row[CH][R];
+  double colc[CH][C];
+  double2 gp[MB][CH][C];
+  double2 gn[MB][CH][C];
+  double w[MB][CH][R];
 };
 template <int MB, bool MSP = false>
 struct Smem {
@@ -215,7 +224,8 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
     const double* colp = &S.colc[0][0] + cl0;
     const double2* gpp = &S.gp[0][0][0] + cl0;
     const double2* gnp = &S.gn[0][0][0] + cl0;
-    const double* wpp = &S.w[0][0][0] + (MSP ? rl0 : 0);
+    const double* wpp = nullptr;
+    if constexpr (MSP) wpp = &S.w[0][0][0] + rl0;
     constexpr int MS = inv::CH * inv::C;  // distance between maps' staging rows
     constexpr int MW = inv::CH * inv::R;  // distance between maps' weight rows (MSP)
 
