@@ -28,9 +28,11 @@
  *     stream (an event hand-off), so concurrent callers never share scratch
  *     in flight.
  *   - Every entry point restores the caller's current CUDA device.
- *   - Band limits: every L >= 1 up to the documented cap L <= 4096 (the FFT
- *     engine keeps one M/2-point half-convolution in an SM's shared memory);
- *     larger L fails with MWSHT_E_DEGREE (UnsupportedDegreeError).
+ *   - Band limits: every L >= 1 up to the documented cap L <= 8192 (the FFT
+ *     engine keeps one H <= 8192-point part of each convolution in an SM's
+ *     shared memory: halves up to L = 4096, quarters above); larger L fails
+ *     with MWSHT_E_DEGREE (UnsupportedDegreeError).  The m-column shard stages
+ *     support L <= 4096.
  *   - `recursion`: MWSHT_TRAPANI or MWSHT_RISBO.  Both are accepted for
  *     drop-in compatibility (mw.py:43,562-566); both run the same stable GPU
  *     recursions (inverse: l-recursion, forward: exponent-scaled Trapani
@@ -58,7 +60,7 @@ typedef enum {
   MWSHT_E_SYMMETRY = 4,     /* SymmetryError           (mw.py:543-547)            */
   MWSHT_E_VALUE = 5,        /* ValueError: unknown recursion (mw.py:562-566)      */
   MWSHT_E_CUDA = 6,         /* CUDA runtime failure                              */
-  MWSHT_E_DEGREE = 7,       /* UnsupportedDegreeError  (errors.py:24-25): L > 4096 */
+  MWSHT_E_DEGREE = 7,       /* UnsupportedDegreeError  (errors.py:24-25): L > 8192 */
   MWSHT_E_NOMEM = 8,        /* device or host allocation failure                 */
   MWSHT_E_PLAN = 9          /* null / mismatched plan                            */
 } mwsht_status;

@@ -208,6 +208,8 @@ struct FftArgs {
   int spread;  // set by the launcher: rows dealt team-major (fft_impl.cuh first_row)
   int msp;                // multi-spin batch: map b's spin parity is bit b of spin_par
   unsigned long long spin_par;
+  int Q;                  // convolution split: M = Q H (2, or 4 for 4096 < L <= 8192)
+  const double2* twM;     // Q = 4: quarter table of w_M (M/4 + 1 entries, global)
 };
 // spin of map `map` as far as the FFT stages need it (its parity)
 __host__ __device__ __forceinline__ int stage_spin(const FftArgs& a, int map) {

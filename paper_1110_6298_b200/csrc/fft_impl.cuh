@@ -329,9 +329,26 @@ __device__ __forceinline__ int first_row(const FftArgs& a, int team) {
   return a.spread ? team * (int)gridDim.x + (int)blockIdx.x : (int)blockIdx.x * NR + team;
 }
 
+// the passes' twiddles w_{2H}^e: quarter table of 2H/4 + 1 entries in smem
+template <int LOGH>
 __device__ __forceinline__ void load_tw(double2* tws, const FftArgs& a) {
-  for (int i = threadIdx.x; i <= a.M / 4; i += kT) tws[i] = a.tw[i];
+  for (int i = threadIdx.x; i <= Cfg<LOGH>::M / 4; i += kT) tws[i] = a.tw[i];
   __syncthreads();
+}
+
+// Quarter split (Q = 4, band limits 4096 < L <= 8192): the M = 4H-point
+// convolution is decimated into four H-point convolutions (radix-4 first
+// step: x_q[j] = w_M^{jq} sum_r x[j + rH] (-i)^{rq}, spectra S_q = DIF_H of
+// the kernel's q-th component) and merged at the end,
+// y[k + pH] = sum_q i^{pq} w_M^{-kq} z_q[k].  w_M^e comes from a global
+// quarter table (twM); z_1..z_3 wait in the team's L2 scratch.
+__device__ __forceinline__ double2 rot_mi(double2 v, int q) {  // v (-i)^q
+  switch (q & 3) {
+    case 0: return v;
+    case 1: return make_double2(v.y, -v.x);
+    case 2: return make_double2(-v.x, -v.y);
+    default: return make_double2(-v.y, v.x);
+  }
 }
 
 __device__ __forceinline__ int fbin(int k, int N) { return k >= 0 ? k : k + N; }
@@ -339,12 +356,43 @@ __device__ __forceinline__ int fbin(int k, int N) { return k >= 0 ? k : k + N; }
 // Bluestein DFT_N of x (fx(n), n < N): forward (conj chirp, spec f) or inverse
 // (chirp, spec i).  Half 1 leaves z1 in scr; half 0 calls fin(k, y_k) with the
 // merged y[k] = z0[k] + w^-k z1[k] (unnormalised; DFT = chirp' . y / M).
-template <int LOGH, bool INV, bool OUTLINE = false, class FX, class FIN>
+template <int LOGH, bool INV, bool OUTLINE = false, int Q = 2, class FX, class FIN>
 __device__ __forceinline__ void bluestein(double2* X, const double2* tw, double2* scr,
                                           const FftArgs& a, int lt, int team, FX fx, FIN fin) {
   using C = Cfg<LOGH>;
   const double2* spec = INV ? a.speci : a.specf;
   const int N = a.N;
+  if constexpr (Q == 4) {
+    // N <= 2H: x[j + rH] is nonzero for r = 0, 1 only; fin(n, y_n) for n < 2H
+    constexpr int H = C::H, MQ = 4 * C::H;
+    auto xv = [&](int n) {
+      double2 v = make_double2(0.0, 0.0);
+      if (n < N) {
+        const double2 c = a.chirp[n];
+        v = INV ? cmul(fx(n), c) : cmulc(fx(n), c);
+      }
+      return v;
+    };
+#pragma unroll 1
+    for (int q = 3; q >= 1; q--) {
+      conv_half<LOGH, OUTLINE>(
+          X, tw, spec + q * H, lt, team,
+          [&](int j) { return cmul(cadd(xv(j), rot_mi(xv(j + H), q)), omega(a.twM, j * q, MQ)); },
+          [&](int k, double2 v) { scr[(q - 1) * H + k] = v; });
+    }
+    conv_half<LOGH, OUTLINE>(
+        X, tw, spec, lt, team, [&](int j) { return cadd(xv(j), xv(j + H)); },
+        [&](int k, double2 z0) {
+          const double2 t1 = cmulc(scr[k], omega(a.twM, k, MQ));
+          const double2 t2 = cmulc(scr[H + k], omega(a.twM, 2 * k, MQ));
+          const double2 t3 = cmulc(scr[2 * H + k], omega(a.twM, 3 * k, MQ));
+          const double2 e = cadd(z0, t2), o = cadd(t1, t3), d = csub(t1, t3);
+          fin(k, cadd(e, o));                                                       // p = 0
+          const double2 ze = csub(z0, t2);
+          fin(k + H, make_double2(ze.x - d.y, ze.y + d.x));                         // p = 1: + i d
+        });
+    return;
+  }
   auto in1 = [&](int j) {
     double2 v = make_double2(0.0, 0.0);
     if (j < N) {
@@ -376,22 +424,38 @@ __device__ __forceinline__ void bluestein(double2* X, const double2* tw, double2
   const int team = threadIdx.x / C::TEAM, lt = threadIdx.x - team * C::TEAM; \
   double2* X = sm + team * C::H;                                             \
   double2* tws = sm + C::NR * C::H;                                          \
-  load_tw(tws, a);                                                           \
+  load_tw<LOGH>(tws, a);                                                     \
   pdl_wait(); /* every access below touches the previous stage's output */   \
-  double2* scr = a.scratch + ((long long)blockIdx.x * C::NR + team) * 3 * C::H;
+  double2* scr = a.scratch + ((long long)blockIdx.x * C::NR + team) * (Q == 4 ? 10 : 3) * C::H;
 
 // ------------------------------------------------------------------ kernels
+// Team scratch (L2): Q = 2: [z1 | F row 0 | F row 1] (3H).  Q = 4: [z1 z2 z3 |
+// Bluestein output y (2H, N <= 2H does not fit the team's H-entry shared row)
+// | F row 0 (2H) | F row 1 (2H) | correlation outputs y[3H + k] (H)] (10H).
+template <int Q, int LOGH>
+struct YStage {  // where a Bluestein output of length N waits for its next pass
+  double2* X;
+  double2* g;
+  __device__ __forceinline__ double2& operator()(int k) const {
+    if constexpr (Q == 4)
+      return g[k];
+    else
+      return X[phys(k)];
+  }
+};
 
 // phi DFT of each ring (forward): AT[k][t] = (2 pi/N) sum_p f[t][p] e^{-2 pi i kp/N}
 // complex: k < N, AT is (N, L); real: k < L (rfft bins), AT is (L, L).
 // Real rings go two per transform: z = f_t + i f_{t+1}, Z = DFT_N(z), then
 // F_t[k] = (Z[k] + conj Z[N-k]) / 2 and F_{t+1}[k] = (Z[k] - conj Z[N-k]) / 2i.
-template <bool REAL, int LOGH, bool SH = false>
+template <bool REAL, int LOGH, bool SH = false, int Q = 2>
 __global__ void __launch_bounds__(kT, 1) k_phi_fwd(FftArgs a) {
   FFT_PROLOGUE
   const int L = a.L, N = a.N;
   const int kout = REAL ? L : N;
-  const double sc = 2.0 * 3.141592653589793 / (double)N / (double)C::M;
+  constexpr int MQ = Q * C::H;  // the convolution length (the DFTs' scale)
+  const YStage<Q, LOGH> ys{X, scr + 3 * C::H};
+  const double sc = 2.0 * 3.141592653589793 / (double)N / (double)MQ;
   const int per_map = REAL ? (a.nrows + 1) / 2 : a.nrows;  // transforms per map
   for (int row = first_row<C::NR>(a, team); row < per_map * a.nmaps; row += gridDim.x * C::NR) {
     const int map = row / per_map, q = row - map * per_map;
@@ -401,16 +465,16 @@ __global__ void __launch_bounds__(kT, 1) k_phi_fwd(FftArgs a) {
       const bool two = tl + 1 < a.nrows;
       const double* f = (const double*)a.in + (long long)map * a.in_stride + (long long)tl * N;
       const double* f2 = two ? f + N : f;
-      bluestein<LOGH, false>(
+      bluestein<LOGH, false, false, Q>(
           X, tws, scr, a, lt, team,
           [&](int n) { return make_double2(f[n], two ? f2[n] : 0.0); },
           [&](int k, double2 y) {
-            if (k < N) X[phys(k)] = cmulc(y, a.chirp[k]);
+            if (k < N) ys(k) = cmulc(y, a.chirp[k]);
           });
       team_sync<C::TEAM>(team);
       const double h = 0.5 * sc;
       for (int k = lt; k < L; k += C::TEAM) {
-        const double2 zk = X[phys(k)], zn = X[phys(k ? N - k : 0)];
+        const double2 zk = ys(k), zn = ys(k ? N - k : 0);
         at[(long long)k * L + t] = make_double2(h * (zk.x + zn.x), h * (zk.y - zn.y));
         if (two) at[(long long)k * L + t + 1] = make_double2(h * (zk.y + zn.y), h * (zn.x - zk.x));
       }
@@ -427,7 +491,7 @@ __global__ void __launch_bounds__(kT, 1) k_phi_fwd(FftArgs a) {
         }
       };
       const double2* f = (const double2*)a.in + (long long)map * a.in_stride + (long long)tl * N;
-      bluestein<LOGH, false>(X, tws, scr, a, lt, team, [&](int n) { return f[n]; }, fin);
+      bluestein<LOGH, false, false, Q>(X, tws, scr, a, lt, team, [&](int n) { return f[n]; }, fin);
     }
   }
 }
@@ -469,12 +533,15 @@ __device__ __forceinline__ int theta_task(int q, int m0, int m1, bool real, int&
 // except at the self-mirrored n = L-1, so its DFT obeys
 //   Z[-k] e^{2 pi i k/N} = eps_m Z[k] + (1 - eps_m) x[L-1] (-1)^k e^{i pi k/N},
 // and with eps_{m+1} = -eps_m the transform of x_m + i x_{m+1} separates.
-template <bool REAL, int LOGH, bool SH = false>
+template <bool REAL, int LOGH, bool SH = false, int Q = 2>
 __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
   FFT_PROLOGUE
-  double2* scrF[2] = {scr + C::H, scr + 2 * C::H};  // F of the task's rows (N <= H)
+  // F of the task's rows (N <= H at Q = 2, N <= 2H at Q = 4)
+  double2* scrF[2] = {scr + (Q == 4 ? 5 : 1) * C::H, scr + (Q == 4 ? 7 : 2) * C::H};
+  double2* y3 = scr + 9 * C::H;  // Q = 4: correlation outputs y[3H + k]
+  const YStage<Q, LOGH> ys{X, scr + 3 * C::H};
   const int L = a.L, N = a.N, ldw = a.ldw;
-  constexpr int H = C::H, M = C::M;
+  constexpr int H = C::H, M = Q * C::H;  // M: the convolution length
   // Two rows per transform from H = 2048 (L >= 513) on, where the rows
   // outnumber the teams; below, every row gets its own team in one wave and
   // the shorter unpaired task (4 instead of 6 half-convolutions) wins
@@ -504,7 +571,7 @@ __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
     };
     // 1. Bluestein DFT_N of the periodic extension(s): X[k] = M Z[k]
     auto ext = [&](int u, int n) { return n < L ? gin(u, n) : cscale(gin(u, 2 * L - 2 - n), eps[u]); };
-    bluestein<LOGH, false, PAIR>(
+    bluestein<LOGH, false, PAIR, Q>(
         X, tws, scr, a, lt, team,
         [&](int n) {
           const double2 x1 = ext(0, n);
@@ -513,7 +580,7 @@ __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
           return make_double2(x1.x - x2.y, x1.y + x2.x);  // x1 + i x2
         },
         [&](int k, double2 y) {
-          if (k < N) X[phys(k)] = cmulc(y, a.chirp[k]);
+          if (k < N) ys(k) = cmulc(y, a.chirp[k]);
         });
     team_sync<C::TEAM>(team);
     // 2. separate the two rows; F[k] = Z[k] tau(f(k)) / (2 pi N)
@@ -541,12 +608,12 @@ __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
         for (int v = 0; v < U; v++) {
           const int k = k0 + v * C::TEAM;
           if (k >= N) break;
-          const double2 zk = X[phys(k)];
+          const double2 zk = ys(k);
           if (!two) {
             scrF[0][k] = cmul(zk, r2[v]);
             continue;
           }
-          const double2 zn = X[phys(k ? N - k : 0)];
+          const double2 zn = ys(k ? N - k : 0);
           const double2 bk = csub(cmul(zn, wk[v]), cmul(cc, ck[v]));
           const double2 eb = cscale(bk, eps[0]);
           const double2 s1 = cadd(zk, eb), s2 = csub(zk, eb);  // 2 Z_1, 2i Z_2
@@ -567,13 +634,38 @@ __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
         if (p >= M - L + 1) return F[p - M + N];
         return make_double2(0.0, 0.0);
       };
-      conv_half<LOGH, PAIR>(
-          X, tws, a.specw + H, lt, team,
-          [&](int j) { return cmul(csub(Fpl(j), Fpl(j + H)), omega(tws, j, M)); },
-          [&](int k, double2 v) { scr[k] = v; });
-      conv_half<LOGH, PAIR>(
-          X, tws, a.specw, lt, team, [&](int j) { return cadd(Fpl(j), Fpl(j + H)); },
-          [&](int k, double2 v) { X[phys(k)] = v; });
+      if constexpr (Q == 4) {
+        // F sits at positions p < L and p > M - L only (L <= H): quarters
+        // r = 0 and r = 3 of the input; the fold needs y[j] and y[M - j] =
+        // y[3H + (H - j)], i.e. the merge's p = 0 and p = 3 outputs
+#pragma unroll 1
+        for (int qq = 3; qq >= 1; qq--) {
+          conv_half<LOGH, PAIR>(
+              X, tws, a.specw + qq * H, lt, team,
+              [&](int j) {
+                return cmul(cadd(Fpl(j), rot_mi(Fpl(j + 3 * H), 3 * qq)), omega(a.twM, j * qq, M));
+              },
+              [&](int k, double2 v) { scr[(qq - 1) * H + k] = v; });
+        }
+        conv_half<LOGH, PAIR>(
+            X, tws, a.specw, lt, team, [&](int j) { return cadd(Fpl(j), Fpl(j + 3 * H)); },
+            [&](int k, double2 z0) {
+              const double2 t1 = cmulc(scr[k], omega(a.twM, k, M));
+              const double2 t2 = cmulc(scr[H + k], omega(a.twM, 2 * k, M));
+              const double2 t3 = cmulc(scr[2 * H + k], omega(a.twM, 3 * k, M));
+              X[phys(k)] = cadd(cadd(z0, t2), cadd(t1, t3));        // y[k]
+              const double2 e = csub(z0, t2), d = csub(t1, t3);
+              y3[k] = make_double2(e.x + d.y, e.y - d.x);          // y[3H + k] = e - i d
+            });
+      } else {
+        conv_half<LOGH, PAIR>(
+            X, tws, a.specw + H, lt, team,
+            [&](int j) { return cmul(csub(Fpl(j), Fpl(j + H)), omega(tws, j, M)); },
+            [&](int k, double2 v) { scr[k] = v; });
+        conv_half<LOGH, PAIR>(
+            X, tws, a.specw, lt, team, [&](int j) { return cadd(Fpl(j), Fpl(j + H)); },
+            [&](int k, double2 v) { X[phys(k)] = v; });
+      }
       team_sync<C::TEAM>(team);
       // 4. G(m') = y[m' mod M]/M; fold gf[j] = G(j) + s G(-j); write staging column
       const double sig = eps[u];  // (-1)^(m+s) (complex) / (-1)^m (real), mw.py:273-285
@@ -581,11 +673,20 @@ __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
       double2* gT =
           (double2*)a.out + (long long)map * a.out_stride + (neg ? (long long)L * ldw : 0);
       for (int j = lt; j < L; j += C::TEAM) {
-        double2 v = cadd(X[phys(j)], cmulc(scr[j], omega(tws, j, M)));
-        if (j > 0) {
-          const int k = H - j;  // position M - j = k + H
-          const double2 w = csub(X[phys(k)], cmulc(scr[k], omega(tws, k, M)));
-          v = make_double2(v.x + sig * w.x, v.y + sig * w.y);
+        double2 v;
+        if constexpr (Q == 4) {
+          v = X[phys(j)];
+          if (j > 0) {
+            const double2 w = y3[H - j];  // y[M - j]
+            v = make_double2(v.x + sig * w.x, v.y + sig * w.y);
+          }
+        } else {
+          v = cadd(X[phys(j)], cmulc(scr[j], omega(tws, j, M)));
+          if (j > 0) {
+            const int k = H - j;  // position M - j = k + H
+            const double2 w = csub(X[phys(k)], cmulc(scr[k], omega(tws, k, M)));
+            v = make_double2(v.x + sig * w.x, v.y + sig * w.y);
+          }
         }
         v = cscale(v, inv);
         if (neg && (j & 1)) v = make_double2(-v.x, -v.y);
@@ -600,12 +701,13 @@ __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
 
 // inverse theta synthesis per order row: rows[t] = sum_m' S[bin(m')] e^{+2 pi i m' t/N}
 // (S already carries the core's twist), keep t < L, write Out[t][col].
-template <bool REAL, int LOGH, bool SH = false>
+template <bool REAL, int LOGH, bool SH = false, int Q = 2>
 __global__ void __launch_bounds__(kT, 1) k_theta_inv(FftArgs a) {
   FFT_PROLOGUE
   const int L = a.L, N = a.N;
   const int ocols = REAL ? L : N;
-  const double inv = 1.0 / (double)C::M;
+  const YStage<Q, LOGH> ys{X, scr + 3 * C::H};
+  const double inv = 1.0 / (double)(Q * C::H);
   const int ntask = theta_tasks(a.m0, a.m1, REAL);
   for (int task = first_row<C::NR>(a, team); task < ntask * a.nmaps; task += gridDim.x * C::NR) {
     const int map = task / ntask, q = task - map * ntask;
@@ -622,7 +724,7 @@ __global__ void __launch_bounds__(kT, 1) k_theta_inv(FftArgs a) {
     }
     const double e1 = (((mr[0] + (REAL ? 0 : stage_spin(a, map))) & 1) ? -1.0 : 1.0);
     double2* o = (double2*)a.out + (long long)map * a.out_stride;
-    bluestein<LOGH, true>(
+    bluestein<LOGH, true, false, Q>(
         X, tws, scr, a, lt, team,
         [&](int n) {
           const double2 s1 = sp[0][n];
@@ -631,7 +733,7 @@ __global__ void __launch_bounds__(kT, 1) k_theta_inv(FftArgs a) {
           return make_double2(s1.x - s2.y, s1.y + s2.x);  // S_1 + i S_2
         },
         [&](int t, double2 y) {
-          if (t < N) X[phys(t)] = cscale(cmul(y, a.chirp[t]), inv);
+          if (t < N) ys(t) = cscale(cmul(y, a.chirp[t]), inv);
         });
     team_sync<C::TEAM>(team);
     // ring t of order row u: dense (L, N) plane, or the shard's send layout
@@ -642,10 +744,10 @@ __global__ void __launch_bounds__(kT, 1) k_theta_inv(FftArgs a) {
         return o[(long long)t * ocols + col[u]];
     };
     for (int t = lt; t < L; t += C::TEAM) {
-      const double2 z = X[phys(t)];
+      const double2 z = ys(t);
       double2 v1 = z;
       if (two) {
-        const double2 zr = cscale(X[phys(N - 1 - t)], e1);
+        const double2 zr = cscale(ys(N - 1 - t), e1);
         v1 = cscale(cadd(z, zr), 0.5);
         const double2 w = csub(z, zr);  // 2i y_2
         oat(t, 1) = make_double2(0.5 * w.y, -0.5 * w.x);
@@ -660,11 +762,11 @@ __global__ void __launch_bounds__(kT, 1) k_theta_inv(FftArgs a) {
 // inverse phi synthesis per ring t: samples[t][p] = sum_m Out[t][bin(m)] e^{+2 pi i m p/N}
 // (real: Hermitian completion of the m >= 0 half, real part out; mw.py:558).
 // Real rings go two per transform: IDFT(X_t + i X_{t+1}) = x_t + i x_{t+1}.
-template <bool REAL, int LOGH, bool SH = false>
+template <bool REAL, int LOGH, bool SH = false, int Q = 2>
 __global__ void __launch_bounds__(kT, 1) k_phi_inv(FftArgs a) {
   FFT_PROLOGUE
   const int L = a.L, N = a.N;
-  const double inv = 1.0 / (double)C::M;
+  const double inv = 1.0 / (double)(Q * C::H);
   const int per_map = REAL ? (a.nrows + 1) / 2 : a.nrows;  // transforms per map
   for (int row = first_row<C::NR>(a, team); row < per_map * a.nmaps; row += gridDim.x * C::NR) {
     const int map = row / per_map, q = row - map * per_map;
@@ -674,7 +776,7 @@ __global__ void __launch_bounds__(kT, 1) k_phi_inv(FftArgs a) {
       const double2* h = (const double2*)a.in + (long long)map * a.in_stride + (long long)t * L;
       const double2* h2 = h + L;
       double* o = (double*)a.out + (long long)map * a.out_stride + (long long)tl * N;
-      bluestein<LOGH, true>(
+      bluestein<LOGH, true, false, Q>(
           X, tws, scr, a, lt, team,
           [&](int n) {
             const double2 x1 = n < L ? h[n] : conjd(h[N - n]);
@@ -699,7 +801,7 @@ __global__ void __launch_bounds__(kT, 1) k_phi_inv(FftArgs a) {
         else
           return h[n];
       };
-      bluestein<LOGH, true>(X, tws, scr, a, lt, team, hin,
+      bluestein<LOGH, true, false, Q>(X, tws, scr, a, lt, team, hin,
                             [&](int p, double2 y) {
                               if (p < N) o[p] = cscale(cmul(y, a.chirp[p]), inv);
                             });
@@ -721,24 +823,33 @@ __device__ __forceinline__ void dif_all(const double2* tw, int lt, LDS lds, STS 
   }
 }
 
-template <int LOGH>
+template <int LOGH, int Q = 2>
 __global__ void __launch_bounds__(kT, 1) k_spectrum(FftArgs a, const double2* kern, double2* spec) {
   FFT_PROLOGUE
   (void)scr;
   if (team != 0) return;
   auto lds = [&](int i) { return X[phys(i)]; };
   auto sts = [&](int i, double2 v) { X[phys(i)] = v; };
-  for (int half = 0; half < 2; half++) {
-    for (int j = lt; j < C::H; j += C::TEAM) {
-      const double2 u = kern[j], v = kern[j + C::H];
-      X[phys(j)] = half ? cmul(csub(u, v), omega(tws, j, C::M)) : cadd(u, v);
+  constexpr int H = C::H, MQ = Q * C::H;
+  for (int part = 0; part < Q; part++) {
+    for (int j = lt; j < H; j += C::TEAM) {
+      double2 v;
+      if constexpr (Q == 4) {  // x_q[j] = w_M^{jq} sum_r kern[j + rH] (-i)^{rq}
+        v = make_double2(0.0, 0.0);
+        for (int r = 0; r < 4; r++) v = cadd(v, rot_mi(kern[j + r * H], r * part));
+        v = cmul(v, omega(a.twM, j * part, MQ));
+      } else {
+        const double2 u = kern[j], w = kern[j + H];
+        v = part ? cmul(csub(u, w), omega(tws, j, C::M)) : cadd(u, w);
+      }
+      X[phys(j)] = v;
     }
     team_sync<C::TEAM>(0);
     dif_all<LOGH, 0>(tws, lt, lds, sts);
     constexpr int RL = 1 << C::lr(C::NP - 1);
-    for (int j = lt; j < C::H; j += C::TEAM) {
+    for (int j = lt; j < H; j += C::TEAM) {
       const int b = j / RL, k = j - b * RL;
-      spec[half * C::H + spec_index<C::H, RL, C::TEAM>(b, k, b % C::TEAM)] = X[phys(j)];
+      spec[part * H + spec_index<C::H, RL, C::TEAM>(b, k, b % C::TEAM)] = X[phys(j)];
     }
     team_sync<C::TEAM>(0);
   }
@@ -773,6 +884,29 @@ static void launch_t(K kern, const FftArgs& a, int nsm, cudaStream_t st) {
 
 template <int LOGH>
 static void launch_stage(int which, bool real, const FftArgs& a, int nsm, cudaStream_t st) {
+  if constexpr (LOGH == 13) {
+    if (a.Q == 4) {  // 4096 < L <= 8192: quarter split (no shard layouts)
+      switch (which) {
+        case 0:
+          real ? launch_t<LOGH>(k_phi_fwd<true, LOGH, false, 4>, a, nsm, st)
+               : launch_t<LOGH>(k_phi_fwd<false, LOGH, false, 4>, a, nsm, st);
+          break;
+        case 1:
+          real ? launch_t<LOGH>(k_theta_fwd<true, LOGH, false, 4>, a, nsm, st)
+               : launch_t<LOGH>(k_theta_fwd<false, LOGH, false, 4>, a, nsm, st);
+          break;
+        case 2:
+          real ? launch_t<LOGH>(k_theta_inv<true, LOGH, false, 4>, a, nsm, st)
+               : launch_t<LOGH>(k_theta_inv<false, LOGH, false, 4>, a, nsm, st);
+          break;
+        default:
+          real ? launch_t<LOGH>(k_phi_inv<true, LOGH, false, 4>, a, nsm, st)
+               : launch_t<LOGH>(k_phi_inv<false, LOGH, false, 4>, a, nsm, st);
+          break;
+      }
+      return;
+    }
+  }
   // SH: the m-column shard exchange layouts (complex maps only)
   const bool sh = !real && (a.row_off || a.col_off);
   switch (which) {
@@ -802,6 +936,13 @@ static void launch_stage(int which, bool real, const FftArgs& a, int nsm, cudaSt
 template <int LOGH>
 static void spectrum_t(const FftArgs& a, const double2* kern, double2* spec, cudaStream_t st) {
   const size_t sm = smem_bytes_t<LOGH>();
+  if constexpr (LOGH == 13) {
+    if (a.Q == 4) {
+      smem_attr_once((const void*)k_spectrum<LOGH, 4>, sm);
+      k_spectrum<LOGH, 4><<<1, kT, sm, st>>>(a, kern, spec);
+      return;
+    }
+  }
   smem_attr_once((const void*)k_spectrum<LOGH>, sm);
   k_spectrum<LOGH><<<1, kT, sm, st>>>(a, kern, spec);
 }

@@ -88,7 +88,8 @@ struct mwsht_plan {
   };
   std::map<std::pair<int, int>, TileSet> range_tiles;  // tiles with c0 in [m0, m1)
   // fused FFT engine (fft.cu): M-point FFT-convolutions in H = M/2 smem halves
-  int M = 0, H = 0, logH = 0, nsm = 0;
+  int M = 0, H = 0, logH = 0, nsm = 0, Q = 2;  // convolution length M = Q H
+  double2* twM = nullptr;                      // Q = 4: quarter table of w_M
   double2 *tw = nullptr, *chirp = nullptr, *specf = nullptr, *speci = nullptr, *specw = nullptr,
           *rho = nullptr, *scratch = nullptr, *cen = nullptr, *wnk = nullptr, *rho2 = nullptr;
   double2 *bufA = nullptr, *bufB = nullptr, *bufG = nullptr;
@@ -521,6 +522,8 @@ static fft::FftArgs fft_args(mwsht_plan* p) {
   a.wnk = p->wnk;
   a.rho2 = p->rho2;
   a.scratch = p->scratch;
+  a.Q = p->Q;
+  a.twM = p->twM;
   a.nmaps = 1;
   a.m0 = 0;
   a.m1 = p->L;
@@ -534,21 +537,37 @@ static int build_fft_tables(mwsht_plan* p) {
   int M = 8;
   while (M < 4 * L - 3 || M < 2 * N - 1) M <<= 1;
   p->M = M;
-  p->H = M / 2;
+  // the convolutions split into Q parts of H <= 8192 complex values, one
+  // team's row in an SM's shared memory: Q = 2 up to L = 4096, Q = 4 up to 8192
+  p->Q = M / 2 <= 8192 ? 2 : 4;
+  p->H = M / p->Q;
   p->logH = 0;
   while ((1 << p->logH) < p->H) p->logH++;
   if (p->H > 8192)
     return fail(MWSHT_E_DEGREE, "plan_create",
-                "band limit above the documented cap L <= 4096 (one FFT half-convolution per SM)");
+                "band limit above the documented cap L <= 8192 (FFT engine: four quarter-"
+                "convolutions of one SM's shared memory each)");
   const ld PI = 3.141592653589793238462643383279502884L;
-  std::vector<double2> tw(M / 4 + 1), ch(N), rho(N), kf(M, make_double2(0, 0)), ki(kf), kw(kf);
+  // passes: quarter table of w_{2H} (= w_M at Q = 2); Q = 4 also w_M (global)
+  const int M2 = 2 * p->H;
+  std::vector<double2> tw(M2 / 4 + 1), ch(N), rho(N), kf(M, make_double2(0, 0)), ki(kf), kw(kf);
   std::vector<double2> cen(N), wnk(N), rho2(N);
-  for (int j = 0; j <= M / 4; j++) {
-    const ld a = -2.0L * PI * (ld)j / (ld)M;
-    tw[j] = make_double2((double)cosl(a), (double)sinl(a));
+  auto quarter_table = [&](int Mt, std::vector<double2>& t) {
+    t.assign(Mt / 4 + 1, make_double2(0, 0));
+    for (int j = 0; j <= Mt / 4; j++) {
+      const ld a = -2.0L * PI * (ld)j / (ld)Mt;
+      t[j] = make_double2((double)cosl(a), (double)sinl(a));
+    }
+    t[0] = make_double2(1.0, 0.0);
+    t[Mt / 4] = make_double2(0.0, -1.0);
+  };
+  quarter_table(M2, tw);
+  if (p->Q == 4) {
+    std::vector<double2> twm;
+    quarter_table(M, twm);
+    int rc2;
+    if ((rc2 = upload(p, &p->twM, twm))) return rc2;
   }
-  tw[0] = make_double2(1.0, 0.0);
-  tw[M / 4] = make_double2(0.0, -1.0);
   std::vector<ld> cr(N), ci(N);
   for (int n = 0; n < N; n++) {
     const long long e = ((long long)n * n) % (2LL * N);  // c[n] = e^{i pi e/N}
@@ -607,8 +626,9 @@ static int build_fft_tables(mwsht_plan* p) {
   int dev;
   CU(cudaGetDevice(&dev));
   CU(cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, dev));
-  // per CTA: NR teams x 3H complex, NR*H <= 8192 for every size (fft.cu Cfg)
-  if ((rc = dev_alloc(p, (void**)&p->scratch, sizeof(double2) * 3 * 8192 * (size_t)p->nsm)))
+  // per CTA: NR teams x (3H at Q = 2, 10H at Q = 4), NR*H <= 8192 (fft_impl.cuh)
+  if ((rc = dev_alloc(p, (void**)&p->scratch,
+                      sizeof(double2) * (p->Q == 4 ? 10 : 3) * 8192 * (size_t)p->nsm)))
     return rc;
   return MWSHT_OK;
 }
@@ -1172,7 +1192,14 @@ int mwsht_forward_stages_z(mwsht_plan* p, const void* samples, void* gfold, int 
   return MWSHT_OK;
 }
 
+static int check_shard_size(mwsht_plan* p) {
+  if (p->Q != 2)
+    return fail(MWSHT_E_DEGREE, "shard", "m-column sharding supports band limits L <= 4096");
+  return MWSHT_OK;
+}
+
 static int check_range(mwsht_plan* p, int m0, int m1) {
+  if (p->Q != 2) return check_shard_size(p);
   if (m0 < 0 || m1 > p->L || m0 >= m1 || (m0 % kTileCols) || ((m1 % kTileCols) && m1 != p->L))
     return fail(MWSHT_E_CONTRACT, "shard", "order range must be [m0, m1) with multiples of 32 (or m1 = L)");
   return MWSHT_OK;
@@ -1182,7 +1209,7 @@ int mwsht_shard_forward_phi(mwsht_plan* p, const void* samples_rows, int t0, int
                             const long long* row_off, void* out, void* stream) {
   DevGuard dg;
   int rc;
-  if ((rc = check_plan(p, dg))) return rc;
+  if ((rc = check_plan(p, dg)) || (rc = check_shard_size(p))) return rc;
   if (t0 < 0 || t1 > p->L || t0 >= t1) return fail(MWSHT_E_CONTRACT, "shard", "bad ring range");
   std::lock_guard<std::mutex> lk(p->mu);
   StreamUse su(p, (cudaStream_t)stream);
@@ -1289,7 +1316,7 @@ int mwsht_shard_inverse_phi(mwsht_plan* p, const void* in, int t0, int t1,
                             void* stream) {
   DevGuard dg;
   int rc;
-  if ((rc = check_plan(p, dg))) return rc;
+  if ((rc = check_plan(p, dg)) || (rc = check_shard_size(p))) return rc;
   if (t0 < 0 || t1 > p->L || t0 >= t1) return fail(MWSHT_E_CONTRACT, "shard", "bad ring range");
   if ((col_off == nullptr) != (col_stride == nullptr))
     return fail(MWSHT_E_CONTRACT, "shard", "col_off and col_stride go together");

@@ -9,9 +9,9 @@ types.  All arithmetic runs in libmwsht.so (hand-written sm_100a kernels,
 including the FFT stages; no cuFFT/cuBLAS) through the C ABI in
 include/mwsht.h; there is no CPU fallback.
 
-Band limits: every L >= 1 up to L = 4096 (the FFT engine's documented cap);
-larger L raises UnsupportedDegreeError (errors.py:24-25) when the plan is
-built.  Calls are reentrant: plans are shared per (L, device), and the
+Band limits: every L >= 1 up to L = 8192 (the FFT engine's documented cap:
+half-split convolutions up to L = 4096, quarter-split above); larger L raises
+UnsupportedDegreeError (errors.py:24-25) when the plan is built.  Calls are reentrant: plans are shared per (L, device), and the
 library orders calls from different threads/streams on the device so they
 never share scratch in flight (include/mwsht.h).
 

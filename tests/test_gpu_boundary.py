@@ -57,7 +57,7 @@ def test_two_threads_two_streams_share_one_plan(mw):
 
 def test_band_limit_above_cap_raises_unsupported_degree(mw):
     import torch
-    L = 4097
+    L = 8193
     with pytest.raises(mw.UnsupportedDegreeError):
         mw.get_plan(L)
     assert torch.cuda.current_device() == 0
