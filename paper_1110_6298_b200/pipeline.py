@@ -44,9 +44,12 @@ KINDS = ("inverse", "forward", "roundtrip")
 
 class HostPipeline:
     def __init__(self, band_limit, spin=0, kind="roundtrip", real=False, device=None,
-                 depth=2, recursion="trapani", fn=None):
+                 depth=2, recursion="trapani", fn=None, batch=None):
         """fn: optional callable (device input) -> device result that replaces
-        the public-API transform(s), e.g. a sharded round trip."""
+        the public-API transform(s), e.g. a sharded round trip.  batch=B: each
+        submission is B maps of one spin (leading dimension B), transformed by
+        forward_batch / inverse_batch, which share every Wigner recursion
+        between maps (complex maps only)."""
         if kind not in KINDS:
             raise ValueError(f"kind must be one of {KINDS}, got {kind!r}")
         if real and spin != 0:
@@ -54,6 +57,9 @@ class HostPipeline:
             raise InvalidSpinError(f"the real-signal path supports spin 0 only, got {spin}")
         if depth < 1:
             raise ValueError("depth must be >= 1")
+        if batch is not None and (real or batch < 1):
+            raise ValueError("batch needs complex maps and batch >= 1")
+        self.batch = batch
         mw.check_band_limit(band_limit)
         self.L, self.spin, self.kind, self.real = band_limit, spin, kind, real
         self.recursion = recursion
@@ -65,6 +71,8 @@ class HostPipeline:
             shape, dtype = (L, N), (torch.float64 if real else torch.complex128)
         else:
             shape, dtype = (L * L,), torch.complex128
+        if batch is not None:
+            shape = (batch,) + shape
         self.in_shape, self.in_dtype = shape, dtype
         self.h2d = torch.cuda.Stream(dev)
         self.d2h = torch.cuda.Stream(dev)
@@ -76,6 +84,11 @@ class HostPipeline:
 
     def _run(self, x):
         L, s, rec = self.L, self.spin, self.recursion
+        if self.batch is not None:
+            if self.kind == "forward":
+                return mw.forward_batch(x, L, s, rec)
+            sig = mw.inverse_batch(x, L, s, rec)
+            return sig if self.kind == "inverse" else mw.forward_batch(sig, L, s, rec)
         if self.kind in ("inverse", "roundtrip"):
             # the l < |spin| zeros were checked on the host copy in submit()
             if self.real:
@@ -112,7 +125,7 @@ class HostPipeline:
             from .errors import ContractViolationError
             raise ContractViolationError(f"pipeline input must have shape {self.in_shape}, "
                                          f"got {tuple(h_in.shape)}")
-        if self.kind != "forward" and self.fn is None and \
+        if self.kind != "forward" and self.fn is None and self.batch is None and \
                 mw._lead_nonzero(h_in.cpu() if h_in.is_cuda else h_in, self.spin * self.spin):
             from .errors import ContractViolationError
             raise ContractViolationError(f"coefficients with degree below |spin|={abs(self.spin)} "

@@ -83,3 +83,29 @@ def test_pipeline_defers_reality_check_to_synchronize():
     assert np.max(np.abs(outs[2].numpy() - ref)) == 0.0
     pipe.submit(good, outs[0])
     pipe.synchronize()  # the error was reported once; the pipeline keeps working
+
+
+def test_pipeline_batched_submissions():
+    # HostPipeline(batch=B): each submission is B maps through forward_batch /
+    # inverse_batch (one recursion shared by the maps); results as per map
+    import numpy as np
+    import torch
+    import paper_1110_6298_b200 as mw
+    from paper_1110_6298_b200.pipeline import HostPipeline
+    from oracle import mw_oracle as O
+    L, s, B = 96, 2, 3
+    vals = np.stack([O.gaussian_coeffs(L, s, 20 + k) for k in range(B)])
+    h_in = torch.from_numpy(vals).pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    h_sig = torch.empty((B, L, 2 * L - 1), dtype=torch.complex128).pin_memory()
+    pipe = HostPipeline(L, s, kind="roundtrip", batch=B)
+    inv = HostPipeline(L, s, kind="inverse", batch=B)
+    for _ in range(3):
+        pipe.submit(h_in, h_out)
+        inv.submit(h_in, h_sig)
+    pipe.synchronize()
+    inv.synchronize()
+    assert float((h_out - h_in).abs().max()) < 1e-12
+    for b in range(B):
+        ref = O.inverse(vals[b], L, s)
+        assert float(np.max(np.abs(h_sig[b].numpy() - ref))) < 1e-12 * float(np.max(np.abs(ref)))
