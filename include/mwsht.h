@@ -31,8 +31,7 @@
  *   - Band limits: every L >= 1 up to the documented cap L <= 8192 (the FFT
  *     engine keeps one H <= 8192-point part of each convolution in an SM's
  *     shared memory: halves up to L = 4096, quarters above); larger L fails
- *     with MWSHT_E_DEGREE (UnsupportedDegreeError).  The m-column shard stages
- *     support L <= 4096.
+ *     with MWSHT_E_DEGREE (UnsupportedDegreeError).
  *   - `recursion`: MWSHT_TRAPANI or MWSHT_RISBO.  Both are accepted for
  *     drop-in compatibility (mw.py:43,562-566); both run the same stable GPU
  *     recursions (inverse: l-recursion, forward: exponent-scaled Trapani

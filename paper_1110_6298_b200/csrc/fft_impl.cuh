@@ -885,23 +885,28 @@ static void launch_t(K kern, const FftArgs& a, int nsm, cudaStream_t st) {
 template <int LOGH>
 static void launch_stage(int which, bool real, const FftArgs& a, int nsm, cudaStream_t st) {
   if constexpr (LOGH == 13) {
-    if (a.Q == 4) {  // 4096 < L <= 8192: quarter split (no shard layouts)
+    if (a.Q == 4) {  // 4096 < L <= 8192: quarter split (and its shard layouts)
+      const bool sh4 = !real && (a.row_off || a.col_off);
       switch (which) {
         case 0:
           real ? launch_t<LOGH>(k_phi_fwd<true, LOGH, false, 4>, a, nsm, st)
-               : launch_t<LOGH>(k_phi_fwd<false, LOGH, false, 4>, a, nsm, st);
+               : sh4 ? launch_t<LOGH>(k_phi_fwd<false, LOGH, true, 4>, a, nsm, st)
+                     : launch_t<LOGH>(k_phi_fwd<false, LOGH, false, 4>, a, nsm, st);
           break;
         case 1:
           real ? launch_t<LOGH>(k_theta_fwd<true, LOGH, false, 4>, a, nsm, st)
-               : launch_t<LOGH>(k_theta_fwd<false, LOGH, false, 4>, a, nsm, st);
+               : sh4 ? launch_t<LOGH>(k_theta_fwd<false, LOGH, true, 4>, a, nsm, st)
+                     : launch_t<LOGH>(k_theta_fwd<false, LOGH, false, 4>, a, nsm, st);
           break;
         case 2:
           real ? launch_t<LOGH>(k_theta_inv<true, LOGH, false, 4>, a, nsm, st)
-               : launch_t<LOGH>(k_theta_inv<false, LOGH, false, 4>, a, nsm, st);
+               : sh4 ? launch_t<LOGH>(k_theta_inv<false, LOGH, true, 4>, a, nsm, st)
+                     : launch_t<LOGH>(k_theta_inv<false, LOGH, false, 4>, a, nsm, st);
           break;
         default:
           real ? launch_t<LOGH>(k_phi_inv<true, LOGH, false, 4>, a, nsm, st)
-               : launch_t<LOGH>(k_phi_inv<false, LOGH, false, 4>, a, nsm, st);
+               : sh4 ? launch_t<LOGH>(k_phi_inv<false, LOGH, true, 4>, a, nsm, st)
+                     : launch_t<LOGH>(k_phi_inv<false, LOGH, false, 4>, a, nsm, st);
           break;
       }
       return;

@@ -1193,13 +1193,11 @@ int mwsht_forward_stages_z(mwsht_plan* p, const void* samples, void* gfold, int 
 }
 
 static int check_shard_size(mwsht_plan* p) {
-  if (p->Q != 2)
-    return fail(MWSHT_E_DEGREE, "shard", "m-column sharding supports band limits L <= 4096");
+  (void)p;  // every supported band limit (quarter-split FFTs included) shards
   return MWSHT_OK;
 }
 
 static int check_range(mwsht_plan* p, int m0, int m1) {
-  if (p->Q != 2) return check_shard_size(p);
   if (m0 < 0 || m1 > p->L || m0 >= m1 || (m0 % kTileCols) || ((m1 % kTileCols) && m1 != p->L))
     return fail(MWSHT_E_CONTRACT, "shard", "order range must be [m0, m1) with multiples of 32 (or m1 = L)");
   return MWSHT_OK;

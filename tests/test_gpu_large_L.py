@@ -135,7 +135,20 @@ def test_real_path_above_4096(mw):
     assert (back - v).abs().max().item() < 2e-11
 
 
-def test_sharding_refuses_above_4096(mw):
+def test_mcolumn_sharding_above_4096(mw):
+    # the m-column shard stages with the quarter-split FFTs (dense-layout
+    # emulation of 2 ranks on one GPU) match the unsharded transform
+    import torch
+    from oracle import mw_oracle as O
     from paper_1110_6298_b200 import shard
-    with pytest.raises(mw.UnsupportedDegreeError):
-        shard.emulate_mcolumn(4500, 2, 0, __import__("torch").zeros(4500 * 4500, dtype=__import__("torch").complex128, device="cuda"))
+    L, spin = 4500, 2
+    v = torch.from_numpy(O.gaussian_coeffs(L, spin, 8)).cuda()
+    samples, flm = shard.emulate_mcolumn(L, 2, spin, v)
+    plan = mw.get_plan(L)
+    plan.set_paired(0)
+    try:
+        ref = mw.inverse(mw.HarmonicCoeffs(L, spin, v)).samples
+    finally:
+        plan.set_paired(-1)
+    assert (samples - ref).abs().max().item() == 0.0
+    assert (flm - v).abs().max().item() < 2e-11
