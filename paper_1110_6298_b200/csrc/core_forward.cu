@@ -50,11 +50,11 @@ struct Stage<MB, true> {
   double2 gn[MB][CH][C];
   double w[MB][CH][R];
 };
-template <int MB, bool MSP = false>
+template <int MB, bool MSP = false, int FW = kConsumerWarps>
 struct Smem {
   static constexpr int NB = MSP ? kStages - 2 : (MB == 1 ? kStages : kStages - 1);
   Stage<MB, MSP> st[NB];
-  double seedy[8][kConsumerThreads];
+  double seedy[2048 / (32 * FW)][32 * FW];  // one seed per chain of the 64 x 32 tile
   uint64_t full[NB], empty[NB];
 };
 }  // namespace fwd
@@ -75,11 +75,15 @@ __device__ __forceinline__ void rescale(double (&y)[NE], double (&y1)[NE], unsig
 
 // Warp-specialised 384-thread CTA (common.cuh): warpgroup 0 = TMA producer,
 // warpgroups 1-2 = 8 consumer warps with a raised register budget.
-template <bool REAL, bool SPIN0, int MB, bool MSP = false>
-__global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
-  constexpr int NI = 4, NJ = 2, NE = NI * NJ;
+// FW consumer warps: 8 (4 x 2 chains per thread, registers raised to 232 with
+// setmaxnreg) or 16 (2 x 2 chains per thread: twice the warps per scheduler
+// to hide the FP64 latency; 96 registers, no register hand-off needed).
+template <bool REAL, bool SPIN0, int MB, bool MSP = false, int FW = kConsumerWarps>
+__global__ void __launch_bounds__(128 + 32 * FW, 1) k_forward_core(FwdArgs a) {
+  constexpr int NI = 32 / FW, NJ = 2, NE = NI * NJ;
+  constexpr int PB = 4 * NI;  // row pairs per warp (a warp's rows share one parity)
   constexpr int NG = REAL ? 1 : 2;
-  using Sm = fwd::Smem<MB, MSP>;
+  using Sm = fwd::Smem<MB, MSP, FW>;
   constexpr int NB = Sm::NB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
@@ -99,7 +103,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
   if (threadIdx.x == 0) {
     for (int b = 0; b < NB; b++) {
       mbar_init(&sm.full[b], 1);
-      mbar_init(&sm.empty[b], kConsumerWarps);
+      mbar_init(&sm.empty[b], FW);
     }
     fence_mbar_init();
   }
@@ -107,7 +111,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
 
   if (wall < 4) {
     // warpgroup 0: warp 0 streams the stages, warps 1-3 retire
-    setmaxnreg_dec<kProducerRegs>();
+    if constexpr (FW == 8) setmaxnreg_dec<kProducerRegs>();
     if (wall != 0) return;
     pdl_wait();  // staged inputs come from the previous kernel
     // ------------------------------------------------------------ producer
@@ -148,14 +152,14 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
   }
 
   // -------------------------------------------------------------- consumers
-  setmaxnreg_inc<kConsumerRegs>();
+  if constexpr (FW == 8) setmaxnreg_inc<kConsumerRegs>();
   const int w = wall - 4, tid = threadIdx.x - 128;
-  const int wr = w & 3, wc = w >> 2, r = lane & 3, c = lane >> 2, par = wr & 1;
+  const int wr = w % (FW / 2), wc = w / (FW / 2), r = lane & 3, c = lane >> 2, par = wr & 1;
   int rl[NI], cl[NJ], ll[NI], mm[NJ];
   double md[NJ];
 #pragma unroll
   for (int i = 0; i < NI; i++) {
-    rl[i] = par + 2 * (16 * (wr >> 1) + 4 * i + r);
+    rl[i] = par + 2 * (PB * (wr >> 1) + 4 * i + r);
     ll[i] = l0b + rl[i];
   }
 #pragma unroll
@@ -201,8 +205,8 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
   unsigned lv = 0;
 
   // warp extents.  Valid chains: m <= l < L; chain (l, m) starts at m' = l.
-  const int wrow_lo = l0b + par + 32 * (wr >> 1);
-  const int wrow_hi = min(wrow_lo + 30, L - 1);
+  const int wrow_lo = l0b + par + 2 * PB * (wr >> 1);
+  const int wrow_hi = min(wrow_lo + 2 * PB - 2, L - 1);
   const int wcol_lo = c0 + 16 * wc;
   const bool warp_has = wrow_lo < L && wcol_lo <= wrow_hi;
   bool fast = false, started = false;
@@ -438,19 +442,39 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_forward_core(FwdArgs a) {
 }
 }
 
-template <bool REAL, bool SPIN0, int MB, bool MSP = false>
+template <bool REAL, bool SPIN0, int MB, bool MSP = false, int FW = kConsumerWarps>
 static void launch_fwd(const FwdArgs& a, int ntiles, cudaStream_t st) {
-  const size_t smem = sizeof(fwd::Smem<MB, MSP>);
-  smem_attr_once((const void*)k_forward_core<REAL, SPIN0, MB, MSP>, smem);
+  const size_t smem = sizeof(fwd::Smem<MB, MSP, FW>);
+  smem_attr_once((const void*)k_forward_core<REAL, SPIN0, MB, MSP, FW>, smem);
   dim3 grid(ntiles, (a.nmaps + MB - 1) / MB);
-  launch_pdl(k_forward_core<REAL, SPIN0, MB, MSP>, grid, dim3(kCoreThreadsWS), smem, st, a);
+  launch_pdl(k_forward_core<REAL, SPIN0, MB, MSP, FW>, grid, dim3(128 + 32 * FW), smem, st, a);
+}
+
+// Consumer warps of the single-map forward core: 16 up to L = 1024 (C3 forward
+// core 0.147 -> 0.128 ms: shorter tiles per warp balance better), 8 above
+// (C5: 7.87 ms vs 8.53 ms with 16).  MWSHT_FWD_CW=8|16 overrides.
+static int fwd_warps(int L) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("MWSHT_FWD_CW");
+    env = e ? atoi(e) : 0;
+  }
+  if (env == 8 || env == 16) return env;
+  return L <= 1024 ? 16 : 8;
 }
 
 template <int MB>
 static void launch_fwd_mb(const FwdArgs& a, int ntiles, bool real, cudaStream_t st) {
-  if (a.msp)  // mixed spins: every m' contracts (no spin-0 parity skip)
+  if (a.msp) {  // mixed spins: every m' contracts (no spin-0 parity skip)
     launch_fwd<false, false, 2, true>(a, ntiles, st);
-  else if (real)
+  } else if (MB == 1 && fwd_warps(a.t.L) == 16) {
+    if (real)
+      launch_fwd<true, true, 1, false, 16>(a, ntiles, st);
+    else if (a.spin == 0)
+      launch_fwd<false, true, 1, false, 16>(a, ntiles, st);
+    else
+      launch_fwd<false, false, 1, false, 16>(a, ntiles, st);
+  } else if (real)
     launch_fwd<true, true, MB>(a, ntiles, st);
   else if (a.spin == 0)
     launch_fwd<false, true, MB>(a, ntiles, st);
