@@ -59,11 +59,11 @@ struct Stage<MB, true> {
   double2 gn[MB][CH][C];
   double w[MB][CH][R];
 };
-template <int MB, bool MSP = false>
+template <int MB, bool MSP = false, int FW = kConsumerWarps>
 struct Smem {
   static constexpr int NB = MSP ? kStages - 2 : (MB == 1 ? kStages : kStages - 1);
   Stage<MB, MSP> st[NB];
-  double seedz[8][kConsumerThreads];
+  double seedz[2048 / (32 * FW)][32 * FW];  // one seed per chain of the 64 x 32 tile
   uint64_t full[NB], empty[NB];
 };
 }  // namespace inv
@@ -82,11 +82,15 @@ __device__ __forceinline__ void rescale(double (&z)[NE], double (&zp)[NE], unsig
   }
 }
 
-template <bool REAL, bool SPIN0, int MB, bool MSP = false>
-__global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
-  constexpr int NI = 4, NJ = 2, NE = NI * NJ;
+// FW consumer warps: 8 (4 x 2 chains per thread, registers raised with
+// setmaxnreg) or 16 (2 x 2 chains per thread, no register hand-off; one map,
+// L <= 1024, as the forward core).
+template <bool REAL, bool SPIN0, int MB, bool MSP = false, int FW = kConsumerWarps>
+__global__ void __launch_bounds__(128 + 32 * FW, 1) k_inverse_core(InvArgs a) {
+  constexpr int NI = 32 / FW, NJ = 2, NE = NI * NJ;
+  constexpr int PB = 4 * NI;  // row pairs per warp (a warp's rows share one parity)
   constexpr int NG = REAL ? 1 : 2;  // complex g values per column: f_{l,m} (+ f_{l,-m})
-  using Sm = inv::Smem<MB, MSP>;
+  using Sm = inv::Smem<MB, MSP, FW>;
   constexpr int NB = Sm::NB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
@@ -106,7 +110,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
   if (threadIdx.x == 0) {
     for (int b = 0; b < NB; b++) {
       mbar_init(&sm.full[b], 1);
-      mbar_init(&sm.empty[b], kConsumerWarps);
+      mbar_init(&sm.empty[b], FW);
     }
     fence_mbar_init();
   }
@@ -114,7 +118,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
 
   if (wall < 4) {
     // warpgroup 0: warp 0 streams the stages, warps 1-3 retire; registers go to the consumers
-    setmaxnreg_dec<kProducerRegs>();
+    if constexpr (FW == 8) setmaxnreg_dec<kProducerRegs>();
     if (wall != 0) return;
     pdl_wait();  // staged inputs come from the previous kernel
     // ------------------------------------------------------------ producer
@@ -154,13 +158,13 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
   }
 
   // -------------------------------------------------------------- consumers
-  setmaxnreg_inc<kConsumerRegs>();
+  if constexpr (FW == 8) setmaxnreg_inc<kConsumerRegs>();
   const int w = wall - 4, tid = threadIdx.x - 128;
-  const int wr = w & 3, wc = w >> 2, r = lane & 3, c = lane >> 2, par = wr & 1;
+  const int wr = w % (FW / 2), wc = w / (FW / 2), r = lane & 3, c = lane >> 2, par = wr & 1;
   int rl[NI], cl[NJ], mp[NI], mm[NJ];
 #pragma unroll
   for (int i = 0; i < NI; i++) {
-    rl[i] = par + 2 * (16 * (wr >> 1) + 4 * i + r);
+    rl[i] = par + 2 * (PB * (wr >> 1) + 4 * i + r);
     mp[i] = r0 + rl[i];
   }
 #pragma unroll
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
   }
   unsigned lv = 0;  // current levels, 4 bits per chain (0 = true scale)
 
-  const int wrow_lo = r0 + par + 32 * (wr >> 1);
+  const int wrow_lo = r0 + par + 2 * PB * (wr >> 1);
   const int wcol_lo = c0 + 16 * wc;
   const bool warp_has = wrow_lo < L && wcol_lo < L;
   const int wl0_min = max(wrow_lo, wcol_lo);
@@ -452,19 +456,39 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core(InvArgs a) {
 }
 }
 
-template <bool REAL, bool SPIN0, int MB, bool MSP = false>
+template <bool REAL, bool SPIN0, int MB, bool MSP = false, int FW = kConsumerWarps>
 static void launch_inv(const InvArgs& a, int ntiles, cudaStream_t st) {
-  const size_t smem = sizeof(inv::Smem<MB, MSP>);
-  smem_attr_once((const void*)k_inverse_core<REAL, SPIN0, MB, MSP>, smem);
+  const size_t smem = sizeof(inv::Smem<MB, MSP, FW>);
+  smem_attr_once((const void*)k_inverse_core<REAL, SPIN0, MB, MSP, FW>, smem);
   dim3 grid(ntiles, (a.nmaps + MB - 1) / MB);
-  launch_pdl(k_inverse_core<REAL, SPIN0, MB, MSP>, grid, dim3(kCoreThreadsWS), smem, st, a);
+  launch_pdl(k_inverse_core<REAL, SPIN0, MB, MSP, FW>, grid, dim3(128 + 32 * FW), smem, st, a);
+}
+
+// Consumer warps of the single-map plain inverse core (MWSHT_INV_CW=8|16
+// overrides): 16 up to L = 320 (C2 inverse core 55.5 -> 53.1 us), 8 above
+// (L = 512 / 1024: 1-3% slower with 16; tools/inv_ab.sh).
+static int inv_warps(int L) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("MWSHT_INV_CW");
+    env = e ? atoi(e) : 0;
+  }
+  if (env == 8 || env == 16) return env;
+  return L <= 320 ? 16 : 8;
 }
 
 template <int MB>
 static void launch_inv_mb(const InvArgs& a, int ntiles, bool real, cudaStream_t st) {
-  if (a.msp)  // mixed spins: every degree contracts (no spin-0 parity skip)
+  if (a.msp) {  // mixed spins: every degree contracts (no spin-0 parity skip)
     launch_inv<false, false, 2, true>(a, ntiles, st);
-  else if (real)
+  } else if (MB == 1 && inv_warps(a.t.L) == 16) {
+    if (real)
+      launch_inv<true, true, 1, false, 16>(a, ntiles, st);
+    else if (a.spin == 0)
+      launch_inv<false, true, 1, false, 16>(a, ntiles, st);
+    else
+      launch_inv<false, false, 1, false, 16>(a, ntiles, st);
+  } else if (real)
     launch_inv<true, true, MB>(a, ntiles, st);
   else if (a.spin == 0)
     launch_inv<false, true, MB>(a, ntiles, st);
