@@ -154,8 +154,13 @@ struct Cfg {
   static constexpr int H = 1 << LOGH;
   static constexpr int M = 2 * H;
   static constexpr int NP = (LOGH + 3) / 4;
-  static constexpr int TEAM = (H / 16) < 32 ? 32 : ((H / 16) > kT ? kT : (H / 16));
-  static constexpr int NR = kT / TEAM;
+  // Small rows (H <= 512, L <= 256): one-warp teams, 4 per 128-thread CTA, with
+  // the team's L2 scratch (z1, F rows: 3H) in shared memory instead -- these
+  // sizes are latency-bound, every global round trip shows
+  static constexpr bool SMEM_SCR = LOGH <= 9;
+  static constexpr int KT = SMEM_SCR ? 128 : kT;  // threads per CTA
+  static constexpr int TEAM = (H / 16) < 32 ? 32 : ((H / 16) > KT ? KT : (H / 16));
+  static constexpr int NR = KT / TEAM;
   static constexpr int lr(int p) { return LOGH / NP + (p < LOGH - (LOGH / NP) * NP ? 1 : 0); }
   static constexpr int n_at(int p) {  // sub-length of DIF pass p
     int n = H;
@@ -332,7 +337,7 @@ __device__ __forceinline__ int first_row(const FftArgs& a, int team) {
 // the passes' twiddles w_{2H}^e: quarter table of 2H/4 + 1 entries in smem
 template <int LOGH>
 __device__ __forceinline__ void load_tw(double2* tws, const FftArgs& a) {
-  for (int i = threadIdx.x; i <= Cfg<LOGH>::M / 4; i += kT) tws[i] = a.tw[i];
+  for (int i = threadIdx.x; i <= Cfg<LOGH>::M / 4; i += Cfg<LOGH>::KT) tws[i] = a.tw[i];
   __syncthreads();
 }
 
@@ -426,7 +431,8 @@ __device__ __forceinline__ void bluestein(double2* X, const double2* tw, double2
   double2* tws = sm + C::NR * C::H;                                          \
   load_tw<LOGH>(tws, a);                                                     \
   pdl_wait(); /* every access below touches the previous stage's output */   \
-  double2* scr = a.scratch + ((long long)blockIdx.x * C::NR + team) * (Q == 4 ? 10 : 3) * C::H;
+  double2* scr = C::SMEM_SCR ? sm + C::NR * C::H + (C::M / 4 + 1) + team * 3 * C::H             \
+                             : a.scratch + ((long long)blockIdx.x * C::NR + team) * (Q == 4 ? 10 : 3) * C::H;
 
 // ------------------------------------------------------------------ kernels
 // Team scratch (L2): Q = 2: [z1 | F row 0 | F row 1] (3H).  Q = 4: [z1 z2 z3 |
@@ -449,7 +455,7 @@ struct YStage {  // where a Bluestein output of length N waits for its next pass
 // Real rings go two per transform: z = f_t + i f_{t+1}, Z = DFT_N(z), then
 // F_t[k] = (Z[k] + conj Z[N-k]) / 2 and F_{t+1}[k] = (Z[k] - conj Z[N-k]) / 2i.
 template <bool REAL, int LOGH, bool SH = false, int Q = 2>
-__global__ void __launch_bounds__(kT, 1) k_phi_fwd(FftArgs a) {
+__global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_phi_fwd(FftArgs a) {
   FFT_PROLOGUE
   const int L = a.L, N = a.N;
   const int kout = REAL ? L : N;
@@ -534,7 +540,7 @@ __device__ __forceinline__ int theta_task(int q, int m0, int m1, bool real, int&
 //   Z[-k] e^{2 pi i k/N} = eps_m Z[k] + (1 - eps_m) x[L-1] (-1)^k e^{i pi k/N},
 // and with eps_{m+1} = -eps_m the transform of x_m + i x_{m+1} separates.
 template <bool REAL, int LOGH, bool SH = false, int Q = 2>
-__global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
+__global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_fwd(FftArgs a) {
   FFT_PROLOGUE
   // F of the task's rows (N <= H at Q = 2, N <= 2H at Q = 4)
   double2* scrF[2] = {scr + (Q == 4 ? 5 : 1) * C::H, scr + (Q == 4 ? 7 : 2) * C::H};
@@ -702,7 +708,7 @@ __global__ void __launch_bounds__(kT, 1) k_theta_fwd(FftArgs a) {
 // inverse theta synthesis per order row: rows[t] = sum_m' S[bin(m')] e^{+2 pi i m' t/N}
 // (S already carries the core's twist), keep t < L, write Out[t][col].
 template <bool REAL, int LOGH, bool SH = false, int Q = 2>
-__global__ void __launch_bounds__(kT, 1) k_theta_inv(FftArgs a) {
+__global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_inv(FftArgs a) {
   FFT_PROLOGUE
   const int L = a.L, N = a.N;
   const int ocols = REAL ? L : N;
@@ -763,7 +769,7 @@ __global__ void __launch_bounds__(kT, 1) k_theta_inv(FftArgs a) {
 // (real: Hermitian completion of the m >= 0 half, real part out; mw.py:558).
 // Real rings go two per transform: IDFT(X_t + i X_{t+1}) = x_t + i x_{t+1}.
 template <bool REAL, int LOGH, bool SH = false, int Q = 2>
-__global__ void __launch_bounds__(kT, 1) k_phi_inv(FftArgs a) {
+__global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_phi_inv(FftArgs a) {
   FFT_PROLOGUE
   const int L = a.L, N = a.N;
   const double inv = 1.0 / (double)(Q * C::H);
@@ -824,7 +830,7 @@ __device__ __forceinline__ void dif_all(const double2* tw, int lt, LDS lds, STS 
 }
 
 template <int LOGH, int Q = 2>
-__global__ void __launch_bounds__(kT, 1) k_spectrum(FftArgs a, const double2* kern, double2* spec) {
+__global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_spectrum(FftArgs a, const double2* kern, double2* spec) {
   FFT_PROLOGUE
   (void)scr;
   if (team != 0) return;
@@ -858,7 +864,8 @@ __global__ void __launch_bounds__(kT, 1) k_spectrum(FftArgs a, const double2* ke
 template <int LOGH>
 size_t smem_bytes_t() {
   using C = Cfg<LOGH>;
-  return sizeof(double2) * ((size_t)C::NR * C::H + C::M / 4 + 1);
+  return sizeof(double2) * ((size_t)C::NR * C::H + C::M / 4 + 1 +
+                            (C::SMEM_SCR ? (size_t)C::NR * 3 * C::H : 0));
 }
 
 template <int LOGH, class K>
@@ -869,9 +876,9 @@ static void launch_t(K kern, const FftArgs& a, int nsm, cudaStream_t st) {
   long long rows = (long long)a.nrows * a.nmaps;
   // resident CTAs per SM, within the per-SM scratch budget (NR * H * occ <= 8192)
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kT, sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::KT, sm);
   if (occ < 1) occ = 1;
-  if (occ * C::NR * C::H > 8192) occ = 8192 / (C::NR * C::H);
+  if (!C::SMEM_SCR && occ * C::NR * C::H > 8192) occ = 8192 / (C::NR * C::H);
   // few rows (small L): one CTA per row on as many SMs as there are rows,
   // rows dealt team-major (first_row); else CTA-major on the resident grid
   FftArgs b = a;
@@ -879,7 +886,7 @@ static void launch_t(K kern, const FftArgs& a, int nsm, cudaStream_t st) {
   long long grid = b.spread ? rows : (rows + C::NR - 1) / C::NR;
   if (grid > (long long)nsm * occ) grid = (long long)nsm * occ;
   if (grid < 1) grid = 1;
-  launch_pdl(kern, dim3((unsigned)grid), dim3(kT), sm, st, b);
+  launch_pdl(kern, dim3((unsigned)grid), dim3(C::KT), sm, st, b);
 }
 
 template <int LOGH>
@@ -944,12 +951,12 @@ static void spectrum_t(const FftArgs& a, const double2* kern, double2* spec, cud
   if constexpr (LOGH == 13) {
     if (a.Q == 4) {
       smem_attr_once((const void*)k_spectrum<LOGH, 4>, sm);
-      k_spectrum<LOGH, 4><<<1, kT, sm, st>>>(a, kern, spec);
+      k_spectrum<LOGH, 4><<<1, Cfg<LOGH>::KT, sm, st>>>(a, kern, spec);
       return;
     }
   }
   smem_attr_once((const void*)k_spectrum<LOGH>, sm);
-  k_spectrum<LOGH><<<1, kT, sm, st>>>(a, kern, spec);
+  k_spectrum<LOGH><<<1, Cfg<LOGH>::KT, sm, st>>>(a, kern, spec);
 }
 
 }  // namespace fft
