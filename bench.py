@@ -42,6 +42,7 @@ Rank 0 only.
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -92,6 +93,19 @@ def stage_bytes(L, real):
     N = 2 * L - 1
     b = 16 * (2 * L * N + (L * N + N * N) + 2 * N * N + (N * N + N * L))
     return b / 2 if real else b
+
+
+def stage_flops(L, real):
+    """Algorithmic FP64 flops of the forward FFT stages per map, counting an
+    n-point complex FFT as 5 n log2 n: the phi DFT_N of L rings, then per
+    order row the theta DFT_N and the weight correlation as one forward and
+    one inverse FFT of the power-of-two length M >= 4L-3 (the weights'
+    spectrum is precomputed).  Real path: half the rows."""
+    N = 2 * L - 1
+    M = 1 << int(math.ceil(math.log2(4 * L - 3)))
+    fft = lambda n: 5.0 * n * math.log2(n)
+    f = L * fft(N) + N * (fft(N) + 2 * fft(M))
+    return f / 2 if real else f
 
 
 def dist_env():
@@ -601,6 +615,8 @@ def summarize(key, wl, r, ws, peak_tf, steps, warmup):
     hbm = measured_peaks().get("hbm_gbs")
     st_gbs = (stage_bytes(L, real) * nm / (r["fwd_stages_ms"] / 1e3) / 1e9
               if r["fwd_stages_ms"] > 0 else None)
+    st_tf = (stage_flops(L, real) * nm / (r["fwd_stages_ms"] / 1e3) / 1e12
+             if r["fwd_stages_ms"] > 0 else None)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": steps,
         "warmup": warmup, "ms_per_step": r["total_ms"] / steps, "higher_is_better": True,
@@ -619,7 +635,10 @@ def summarize(key, wl, r, ws, peak_tf, steps, warmup):
                          "forward_fft_stages": {
                              "ms": r["fwd_stages_ms"], "gbs": st_gbs, "hbm_peak_gbs": hbm,
                              "frac": (st_gbs / hbm) if (st_gbs and hbm) else None,
-                             "bytes": "SURVEY §8(d) stage bytes, core term excluded"}}},
+                             "bytes": "SURVEY §8(d) stage bytes, core term excluded",
+                             "fp64_tflops": st_tf,
+                             "fp64_frac": (st_tf / peak_tf) if (st_tf and peak_tf) else None,
+                             "flops": "5 n log2 n per FFT (bench.stage_flops)"}}},
         "gpu_launches": r["launches"] * steps,
         "roundtrip_max_abs_err": r["roundtrip_err"],
         "clocks": r["clocks"],
