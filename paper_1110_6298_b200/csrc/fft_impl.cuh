@@ -705,6 +705,313 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_fwd(FftArgs a) {
   }
 }
 
+// ------------------------------------------------------------- tensor memory
+// The decoupled kernels park thread-private rows in the SM's 256 KB of tensor
+// memory (512 columns x 128 lanes x 32 bit) instead of L2: a warp reaches the
+// 32 lanes of its quarter (warp % 4) with tcgen05.ld/st.32x32b, one lane per
+// thread, so a thread's 16 complex values of a parked row are 64 consecutive
+// columns of its own lane.  The four warps of a lane quarter take 128 columns
+// each: two parked rows per team (slots 0 and 1).  No tensor-core instruction
+// is involved; this is TMEM as a 12-cycle scratchpad (B300_MICROARCH.md).
+struct Tmem {
+  uint32_t base;  // this thread's warp: lane quarter + 128-column window
+  __device__ __forceinline__ uint32_t at(int slot, int r) const { return base + slot * 64 + r * 4; }
+  // four consecutive complex values (16 columns) per instruction
+  __device__ __forceinline__ void st4(int slot, int r, const double2 (&v)[4]) const {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(at(slot, r)),
+        "r"(__double2loint(v[0].x)), "r"(__double2hiint(v[0].x)), "r"(__double2loint(v[0].y)),
+        "r"(__double2hiint(v[0].y)), "r"(__double2loint(v[1].x)), "r"(__double2hiint(v[1].x)),
+        "r"(__double2loint(v[1].y)), "r"(__double2hiint(v[1].y)), "r"(__double2loint(v[2].x)),
+        "r"(__double2hiint(v[2].x)), "r"(__double2loint(v[2].y)), "r"(__double2hiint(v[2].y)),
+        "r"(__double2loint(v[3].x)), "r"(__double2hiint(v[3].x)), "r"(__double2loint(v[3].y)),
+        "r"(__double2hiint(v[3].y))
+        : "memory");
+  }
+  __device__ __forceinline__ void ld4(int slot, int r, double2 (&v)[4]) const {
+    int w[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+          "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]),
+          "=r"(w[14]), "=r"(w[15])
+        : "r"(at(slot, r))
+        : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+      v[i] = make_double2(__hiloint2double(w[4 * i + 1], w[4 * i]),
+                          __hiloint2double(w[4 * i + 3], w[4 * i + 2]));
+  }
+  __device__ __forceinline__ void st_wait() const {
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+};
+// whole-CTA: warp 0 allocates all 512 columns (one CTA per SM: these kernels
+// fill the SM's shared memory), every thread gets its window
+__device__ __forceinline__ Tmem tmem_open(uint32_t* slot) {
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t warp = threadIdx.x >> 5;
+  return Tmem{*slot + (((warp & 3u) * 32u) << 16) + (warp >> 2) * 128u};
+}
+__device__ __forceinline__ void tmem_close(uint32_t* slot) {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(*slot) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Decoupled form of the stage kernels (H >= 2048): every half-convolution runs
+// ALL its passes on the team's shared row through one out-of-line copy
+// (conv_smem), and everything that touches global memory is a short
+// element-wise loop over the 16 row positions a thread OWNS,
+//   pos(r) = lt + r TEAM (r < 8),   H - (lt + (r-8) TEAM) (r >= 8; H/2 for 0),
+// so positions j and H - j (the fold's partners) belong to one thread and the
+// rows that wait between passes (the half-1 result z1, the first pass's input
+// for half 0, the second row's F) are thread-private "parked" arrays in the
+// team's L2 scratch, written and read back coalesced by the same thread.
+// The loops issue their independent loads in batches, so a global round trip
+// is paid once per loop instead of inside a radix-16 butterfly's register
+// budget, and the kernel is a third of the fused form's code size.
+template <int LOGH>
+__device__ __noinline__ void conv_smem(double2* X, const double2* tw, const double2* S, int lt,
+                                       int team) {
+  using C = Cfg<LOGH>;
+  auto lds = [&](int i) { return X[phys(i)]; };
+  auto sts = [&](int i, double2 v) { X[phys(i)] = v; };
+  constexpr int RL = 1 << C::lr(C::NP - 1), nL = C::n_at(C::NP - 1);
+  team_sync<C::TEAM>(team);
+  dif_chain<LOGH, 0>(tw, lt, team, lds, lds, sts);
+  pass<RL, 2, C::H, C::M, nL, C::TEAM>(tw, S, lt, lds, sts);
+  team_sync<C::TEAM>(team);
+  dit_chain<LOGH, C::NP - 2>(tw, lt, team, sts, lds, sts);
+}
+
+template <int LOGH>
+struct Own {
+  using C = Cfg<LOGH>;
+  static constexpr int E = C::H / C::TEAM;  // positions per thread (16)
+  static constexpr int B = 4;               // loads in flight per array and batch
+  __device__ static __forceinline__ int pos(int r, int lt) {
+    if (r < E / 2) return lt + r * C::TEAM;
+    const int q = lt + (r - E / 2) * C::TEAM;
+    return q ? C::H - q : C::H / 2;
+  }
+};
+
+template <bool REAL, int LOGH>
+__global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_fwd2(FftArgs a) {
+  constexpr int Q = 2;
+  __shared__ uint32_t tmem_slot;
+  FFT_PROLOGUE
+  using O = Own<LOGH>;
+  constexpr int H = C::H, M = 2 * C::H, T = C::TEAM, E = O::E, B = O::B;
+  static_assert(E == 16 && B == 4, "16 positions per thread, parked four at a time");
+  // parked rows: TMEM slot 0 = Bluestein input / F of the running row,
+  // slot 1 = z1 of the running convolution; L2 scratch: F of the second row
+  const Tmem tm = tmem_open(&tmem_slot);
+  double2* const PC = scr;
+  const int L = a.L, N = a.N, ldw = a.ldw;
+  const int ntask = theta_tasks(a.m0, a.m1, REAL);
+  for (int task = first_row<C::NR>(a, team); task < ntask * a.nmaps; task += gridDim.x * C::NR) {
+    const int map = task / ntask, q = task - map * ntask;
+    int i1 = q;
+    const bool two = theta_task(q, a.m0, a.m1, REAL, i1) == 2;
+    int mr[2];
+    double eps[2];
+    const double2* g[2];
+    for (int u = 0; u < 2; u++) {
+      mr[u] = row_order(two ? i1 + u : i1, a.m0, a.m1, REAL);
+      eps[u] = (((mr[u] + (REAL ? 0 : stage_spin(a, map))) & 1) ? -1.0 : 1.0);
+      g[u] = (const double2*)a.in + (long long)map * a.in_stride +
+             (long long)(REAL ? mr[u] : fbin(mr[u], N)) * L;
+    }
+    // A. Bluestein input xb[n] = (x_1 + i x_2)[n] conj(c[n]) of the extended rows:
+    //    parked for half 0, times w^n into the row for half 1
+#pragma unroll
+    for (int r0 = 0; r0 < E; r0 += B) {
+      double2 x1[B], x2[B], ch[B];
+#pragma unroll
+      for (int v = 0; v < B; v++) {
+        const int n = min(O::pos(r0 + v, lt), N - 1), src = n < L ? n : 2 * L - 2 - n;
+        x1[v] = g[0][src];
+        x2[v] = two ? g[1][src] : make_double2(0.0, 0.0);
+        ch[v] = a.chirp[n];
+      }
+#pragma unroll
+      for (int v = 0; v < B; v++) {
+        const int p = O::pos(r0 + v, lt);
+        double2 xb = make_double2(0.0, 0.0);
+        if (p < N) {
+          const double e0 = p < L ? 1.0 : eps[0], e1 = p < L ? 1.0 : eps[1];
+          xb = cmulc(make_double2(e0 * x1[v].x - e1 * x2[v].y, e0 * x1[v].y + e1 * x2[v].x), ch[v]);
+        }
+        x1[v] = xb;
+        X[phys(p)] = cmul(xb, omega(tws, p, M));
+      }
+      tm.st4(0, r0, x1);
+    }
+    tm.st_wait();
+    conv_smem<LOGH>(X, tws, a.specf + H, lt, team);
+    // C. park z1, refill the row with the parked input
+#pragma unroll
+    for (int r0 = 0; r0 < E; r0 += B) {
+      double2 xa[B], z1[B];
+      tm.ld4(0, r0, xa);
+#pragma unroll
+      for (int v = 0; v < B; v++) {
+        const int pp = phys(O::pos(r0 + v, lt));
+        z1[v] = X[pp];
+        X[pp] = xa[v];
+      }
+      tm.st4(1, r0, z1);
+    }
+    tm.st_wait();
+    conv_smem<LOGH>(X, tws, a.specf, lt, team);
+    // E. merge the halves: M Z[k] = (z0[k] + conj(w^k) z1[k]) conj(c[k]), k < N, in place
+#pragma unroll
+    for (int r0 = 0; r0 < E; r0 += B) {
+      double2 zb[B], ch[B];
+#pragma unroll
+      for (int v = 0; v < B; v++) ch[v] = a.chirp[min(O::pos(r0 + v, lt), N - 1)];
+      tm.ld4(1, r0, zb);
+#pragma unroll
+      for (int v = 0; v < B; v++) {
+        const int p = O::pos(r0 + v, lt), pp = phys(p);
+        if (p < N) X[pp] = cmulc(cadd(X[pp], cmulc(zb[v], omega(tws, p, M))), ch[v]);
+      }
+    }
+    team_sync<C::TEAM>(team);
+    // F. separate the two rows; F[k] = Z[k] tau(f(k)) / (2 pi N), parked at the
+    //    position the weight correlation wants bin k: k (k < L), k + H - N (k >= L)
+    {
+      double2 cc = make_double2(0.0, 0.0);  // M (1 - eps_u) x_u[L-1] (i for the second row)
+      if (two) {
+        const double2 c1 = g[0][L - 1], c2 = g[1][L - 1];
+        cc = eps[0] < 0 ? make_double2(2.0 * M * c1.x, 2.0 * M * c1.y)
+                        : make_double2(-2.0 * M * c2.y, 2.0 * M * c2.x);
+      }
+#pragma unroll
+      for (int r0 = 0; r0 < E; r0 += B) {
+        double2 r2[B], wk[B], ck[B], f0[B];
+        int kk[B];
+#pragma unroll
+        for (int v = 0; v < B; v++) {
+          const int j = O::pos(r0 + v, lt);
+          kk[v] = r0 + v < E / 2 ? (j < L ? j : -1) : (j >= H - L + 1 ? j - H + N : -1);
+          const int k = max(kk[v], 0);
+          r2[v] = __ldg(&a.rho2[k]);
+          if (two) {
+            wk[v] = __ldg(&a.wnk[k]);
+            ck[v] = __ldg(&a.cen[k]);
+          }
+        }
+#pragma unroll
+        for (int v = 0; v < B; v++) {
+          const int k = kk[v];
+          double2 f1 = make_double2(0.0, 0.0);
+          f0[v] = f1;
+          if (k >= 0) {
+            const double2 zk = X[phys(k)];
+            if (!two) {
+              f0[v] = cmul(zk, r2[v]);
+            } else {
+              const double2 zn = X[phys(k ? N - k : 0)];
+              const double2 eb = cscale(csub(cmul(zn, wk[v]), cmul(cc, ck[v])), eps[0]);
+              const double2 s1 = cadd(zk, eb), s2 = csub(zk, eb);  // 2 Z_1, 2i Z_2
+              f0[v] = cscale(cmul(s1, r2[v]), 0.5);
+              f1 = cscale(cmul(make_double2(s2.y, -s2.x), r2[v]), 0.5);
+            }
+          }
+          if (two) PC[(r0 + v) * T + lt] = f1;
+        }
+        tm.st4(0, r0, f0);
+      }
+      tm.st_wait();
+    }
+    team_sync<C::TEAM>(team);
+    for (int u = 0; u < (two ? 2 : 1); u++) {
+      const int m = mr[u];
+      const bool neg = !REAL && m < 0;
+      const int am = neg ? -m : m;
+      // G. half 1 of the weight correlation: (F(j) - F(j + H)) w^j (the two never overlap)
+#pragma unroll
+      for (int r0 = 0; r0 < E; r0 += B) {
+        double2 f[B];
+        if (u == 0) {
+          tm.ld4(0, r0, f);
+        } else {
+#pragma unroll
+          for (int v = 0; v < B; v++) f[v] = PC[(r0 + v) * T + lt];
+          tm.st4(0, r0, f);
+        }
+#pragma unroll
+        for (int v = 0; v < B; v++) {
+          const int p = O::pos(r0 + v, lt);
+          const double2 w = cmul(f[v], omega(tws, p, M));
+          X[phys(p)] = r0 + v < E / 2 ? w : make_double2(-w.x, -w.y);
+        }
+      }
+      tm.st_wait();
+      conv_smem<LOGH>(X, tws, a.specw + H, lt, team);
+      // I. park z1, refill with F for half 0
+#pragma unroll
+      for (int r0 = 0; r0 < E; r0 += B) {
+        double2 f[B], z1[B];
+        tm.ld4(0, r0, f);
+#pragma unroll
+        for (int v = 0; v < B; v++) {
+          const int pp = phys(O::pos(r0 + v, lt));
+          z1[v] = X[pp];
+          X[pp] = f[v];
+        }
+        tm.st4(1, r0, z1);
+      }
+      tm.st_wait();
+      conv_smem<LOGH>(X, tws, a.specw, lt, team);
+      // K. G(m') = y[m' mod M]/M, y[j] = z0[j] + conj(w^j) z1[j], y[M - j] = z0[H-j] -
+      //    conj(w^(H-j)) z1[H-j]; fold gf[j] = G(j) + s G(-j); write the staging column
+      const double sig = eps[u], inv = 1.0 / (double)M;
+      double2* gT =
+          (double2*)a.out + (long long)map * a.out_stride + (neg ? (long long)L * ldw : 0);
+#pragma unroll
+      for (int r0 = 0; r0 < E / 2; r0 += B) {
+        double2 za[B], zp[B];
+        tm.ld4(1, r0, za);
+        tm.ld4(1, r0 + E / 2, zp);
+#pragma unroll
+        for (int v = 0; v < B; v++) {
+          const int j = lt + (r0 + v) * T;
+          if (j >= L) continue;
+          double2 y = cadd(X[phys(j)], cmulc(za[v], omega(tws, j, M)));
+          if (j > 0) {
+            const int k = H - j;
+            const double2 w = csub(X[phys(k)], cmulc(zp[v], omega(tws, k, M)));
+            y = make_double2(y.x + sig * w.x, y.y + sig * w.y);
+          }
+          y = cscale(y, inv);
+          if (neg && (j & 1)) y = make_double2(-y.x, -y.y);
+          gT[blk<kTileCols>(j, am, L)] = y;
+          if (!REAL && m == 0)
+            gT[(long long)L * ldw + blk<kTileCols>(j, 0, L)] = (j & 1) ? make_double2(-y.x, -y.y) : y;
+        }
+      }
+    }
+  }
+  tmem_close(&tmem_slot);
+}
+
 // inverse theta synthesis per order row: rows[t] = sum_m' S[bin(m')] e^{+2 pi i m' t/N}
 // (S already carries the core's twist), keep t < L, write Out[t][col].
 template <bool REAL, int LOGH, bool SH = false, int Q = 2>
@@ -868,6 +1175,15 @@ size_t smem_bytes_t() {
                             (C::SMEM_SCR ? (size_t)C::NR * 3 * C::H : 0));
 }
 
+// MWSHT_FFT_DECOUPLED=0 falls back to the fused first/last passes (A/B)
+inline bool decoupled_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MWSHT_FFT_DECOUPLED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int LOGH, class K>
 static void launch_t(K kern, const FftArgs& a, int nsm, cudaStream_t st) {
   using C = Cfg<LOGH>;
@@ -928,6 +1244,13 @@ static void launch_stage(int which, bool real, const FftArgs& a, int nsm, cudaSt
                 : launch_t<LOGH>(k_phi_fwd<false, LOGH>, a, nsm, st);
       break;
     case 1:
+      if constexpr (LOGH >= 11) {
+        if (!sh && decoupled_enabled()) {
+          real ? launch_t<LOGH>(k_theta_fwd2<true, LOGH>, a, nsm, st)
+               : launch_t<LOGH>(k_theta_fwd2<false, LOGH>, a, nsm, st);
+          break;
+        }
+      }
       real ? launch_t<LOGH>(k_theta_fwd<true, LOGH>, a, nsm, st)
            : sh ? launch_t<LOGH>(k_theta_fwd<false, LOGH, true>, a, nsm, st)
                 : launch_t<LOGH>(k_theta_fwd<false, LOGH>, a, nsm, st);
