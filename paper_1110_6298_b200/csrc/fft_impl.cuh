@@ -810,7 +810,7 @@ struct Own {
   }
 };
 
-template <bool REAL, int LOGH>
+template <bool REAL, int LOGH, bool SH = false>
 __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_fwd2(FftArgs a) {
   constexpr int Q = 2;
   __shared__ uint32_t tmem_slot;
@@ -828,15 +828,23 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_fwd2(FftArgs a) {
     const int map = task / ntask, q = task - map * ntask;
     int i1 = q;
     const bool two = theta_task(q, a.m0, a.m1, REAL, i1) == 2;
-    int mr[2];
+    int mr[2], il[2];
     double eps[2];
     const double2* g[2];
     for (int u = 0; u < 2; u++) {
-      mr[u] = row_order(two ? i1 + u : i1, a.m0, a.m1, REAL);
+      il[u] = two ? i1 + u : i1;
+      mr[u] = row_order(il[u], a.m0, a.m1, REAL);
       eps[u] = (((mr[u] + (REAL ? 0 : stage_spin(a, map))) & 1) ? -1.0 : 1.0);
       g[u] = (const double2*)a.in + (long long)map * a.in_stride +
              (long long)(REAL ? mr[u] : fbin(mr[u], N)) * L;
     }
+    // ring t of row u: dense AT row, or the shard's receive layout
+    auto gin = [&](int u, int t) -> double2 {
+      if constexpr (SH)
+        return ((const double2*)a.in)[a.col_off[t] + (long long)il[u] * a.col_stride[t]];
+      else
+        return g[u][t];
+    };
     // A. Bluestein input xb[n] = (x_1 + i x_2)[n] conj(c[n]) of the extended rows:
     //    parked for half 0, times w^n into the row for half 1
 #pragma unroll
@@ -845,8 +853,8 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_fwd2(FftArgs a) {
 #pragma unroll
       for (int v = 0; v < B; v++) {
         const int n = min(O::pos(r0 + v, lt), N - 1), src = n < L ? n : 2 * L - 2 - n;
-        x1[v] = g[0][src];
-        x2[v] = two ? g[1][src] : make_double2(0.0, 0.0);
+        x1[v] = gin(0, src);
+        x2[v] = two ? gin(1, src) : make_double2(0.0, 0.0);
         ch[v] = a.chirp[n];
       }
 #pragma unroll
@@ -898,7 +906,7 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_fwd2(FftArgs a) {
     {
       double2 cc = make_double2(0.0, 0.0);  // M (1 - eps_u) x_u[L-1] (i for the second row)
       if (two) {
-        const double2 c1 = g[0][L - 1], c2 = g[1][L - 1];
+        const double2 c1 = gin(0, L - 1), c2 = gin(1, L - 1);
         cc = eps[0] < 0 ? make_double2(2.0 * M * c1.x, 2.0 * M * c1.y)
                         : make_double2(-2.0 * M * c2.y, 2.0 * M * c2.x);
       }
@@ -1245,9 +1253,10 @@ static void launch_stage(int which, bool real, const FftArgs& a, int nsm, cudaSt
       break;
     case 1:
       if constexpr (LOGH >= 11) {
-        if (!sh && decoupled_enabled()) {
+        if (decoupled_enabled()) {
           real ? launch_t<LOGH>(k_theta_fwd2<true, LOGH>, a, nsm, st)
-               : launch_t<LOGH>(k_theta_fwd2<false, LOGH>, a, nsm, st);
+               : sh ? launch_t<LOGH>(k_theta_fwd2<false, LOGH, true>, a, nsm, st)
+                    : launch_t<LOGH>(k_theta_fwd2<false, LOGH>, a, nsm, st);
           break;
         }
       }
