@@ -11,7 +11,8 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("L,spin,world", [(256, 2, 2), (256, 0, 3), (300, -1, 4), (96, 0, 2)])
+@pytest.mark.parametrize("L,spin,world", [(256, 2, 2), (256, 0, 3), (300, -1, 4), (96, 0, 2),
+                                            (600, 1, 2), (1100, 0, 3)])  # H >= 2048: decoupled theta stage
 def test_mcolumn_emulation_matches_unsharded(L, spin, world):
     import torch
     import paper_1110_6298_b200 as mw
