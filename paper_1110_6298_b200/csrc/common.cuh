@@ -185,7 +185,12 @@ struct FftArgs {
   const double2* specf;   // forward Bluestein spectrum, halves [0,H) and [H,2H) (DFT_M of c)
   const double2* speci;   // inverse Bluestein spectrum (DFT_M of conj c)
   const double2* specw;   // weight-correlation spectrum (DFT_M of K'), 2pi included
-  const double2* rho;     // forward theta glue: conj(c[k]) tau(f(k)) / M  (k < N)
+  // decoupled forward theta stage (two rows per transform), with y the Bluestein
+  // output before its chirp: F_1[k] = a + b, F_2[k] = -i (a - b), a = y[k] sep1[k],
+  // b = eps_1 (y[N-k] sep2[k] - cc sep3[k]); one row: F[k] = 2 y[k] sep1[k]
+  const double2* sep1;    // tau(f(k)) conj(c[k]) / (4 pi N M)
+  const double2* sep2;    // tau(f(k)) e^{2 pi i k/N} conj(c[(N-k) mod N]) / (4 pi N M)
+  const double2* sep3;    // tau(f(k)) (-1)^k e^{i pi k/N} / (4 pi N M)
   const double2* cen;     // paired forward theta rows: (-1)^k e^{i pi k/N}  (k < N)
   const double2* wnk;     //                            e^{2 pi i k/N}       (k < N)
   const double2* rho2;    //                            tau(f(k)) / (2 pi N M)

@@ -552,6 +552,8 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_fwd(FftArgs a) {
   // outnumber the teams; below, every row gets its own team in one wave and
   // the shorter unpaired task (4 instead of 6 half-convolutions) wins
   // (L=64: 79 -> 46 us, L=256: 128 -> 74 us per launch).
+  // (at Q = 2 the sizes H >= 2048 run k_theta_fwd2, the decoupled form of the
+  // paired task; this fused paired form serves the quarter split, Q = 4)
   constexpr bool PAIR = LOGH >= 11;
   const int ntask = PAIR ? theta_tasks(a.m0, a.m1, REAL) : a.nrows;
   for (int task = first_row<C::NR>(a, team); task < ntask * a.nmaps; task += gridDim.x * C::NR) {
@@ -887,21 +889,20 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_fwd2(FftArgs a) {
     }
     tm.st_wait();
     conv_smem<LOGH>(X, tws, a.specf, lt, team);
-    // E. merge the halves: M Z[k] = (z0[k] + conj(w^k) z1[k]) conj(c[k]), k < N, in place
+    // E. merge the halves in place: y[k] = z0[k] + conj(w^k) z1[k], k < N (the
+    //    output chirp is folded into the separation tables)
 #pragma unroll
     for (int r0 = 0; r0 < E; r0 += B) {
-      double2 zb[B], ch[B];
-#pragma unroll
-      for (int v = 0; v < B; v++) ch[v] = a.chirp[min(O::pos(r0 + v, lt), N - 1)];
+      double2 zb[B];
       tm.ld4(1, r0, zb);
 #pragma unroll
       for (int v = 0; v < B; v++) {
         const int p = O::pos(r0 + v, lt), pp = phys(p);
-        if (p < N) X[pp] = cmulc(cadd(X[pp], cmulc(zb[v], omega(tws, p, M))), ch[v]);
+        if (p < N) X[pp] = cadd(X[pp], cmulc(zb[v], omega(tws, p, M)));
       }
     }
     team_sync<C::TEAM>(team);
-    // F. separate the two rows; F[k] = Z[k] tau(f(k)) / (2 pi N), parked at the
+    // F. separate the two rows (common.cuh, sep1..3); F[k] is parked at the
     //    position the weight correlation wants bin k: k (k < L), k + H - N (k >= L)
     {
       double2 cc = make_double2(0.0, 0.0);  // M (1 - eps_u) x_u[L-1] (i for the second row)
@@ -912,17 +913,17 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_fwd2(FftArgs a) {
       }
 #pragma unroll
       for (int r0 = 0; r0 < E; r0 += B) {
-        double2 r2[B], wk[B], ck[B], f0[B];
+        double2 t1[B], t2[B], t3[B], f0[B];
         int kk[B];
 #pragma unroll
         for (int v = 0; v < B; v++) {
           const int j = O::pos(r0 + v, lt);
           kk[v] = r0 + v < E / 2 ? (j < L ? j : -1) : (j >= H - L + 1 ? j - H + N : -1);
           const int k = max(kk[v], 0);
-          r2[v] = __ldg(&a.rho2[k]);
+          t1[v] = __ldg(&a.sep1[k]);
           if (two) {
-            wk[v] = __ldg(&a.wnk[k]);
-            ck[v] = __ldg(&a.cen[k]);
+            t2[v] = __ldg(&a.sep2[k]);
+            t3[v] = __ldg(&a.sep3[k]);
           }
         }
 #pragma unroll
@@ -931,15 +932,15 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_fwd2(FftArgs a) {
           double2 f1 = make_double2(0.0, 0.0);
           f0[v] = f1;
           if (k >= 0) {
-            const double2 zk = X[phys(k)];
+            const double2 av = cmul(X[phys(k)], t1[v]);
             if (!two) {
-              f0[v] = cmul(zk, r2[v]);
+              f0[v] = make_double2(2.0 * av.x, 2.0 * av.y);
             } else {
-              const double2 zn = X[phys(k ? N - k : 0)];
-              const double2 eb = cscale(csub(cmul(zn, wk[v]), cmul(cc, ck[v])), eps[0]);
-              const double2 s1 = cadd(zk, eb), s2 = csub(zk, eb);  // 2 Z_1, 2i Z_2
-              f0[v] = cscale(cmul(s1, r2[v]), 0.5);
-              f1 = cscale(cmul(make_double2(s2.y, -s2.x), r2[v]), 0.5);
+              const double2 bv =
+                  cscale(csub(cmul(X[phys(k ? N - k : 0)], t2[v]), cmul(cc, t3[v])), eps[0]);
+              f0[v] = cadd(av, bv);
+              const double2 d = csub(av, bv);
+              f1 = make_double2(d.y, -d.x);  // -i (a - b)
             }
           }
           if (two) PC[(r0 + v) * T + lt] = f1;
@@ -1183,15 +1184,6 @@ size_t smem_bytes_t() {
                             (C::SMEM_SCR ? (size_t)C::NR * 3 * C::H : 0));
 }
 
-// MWSHT_FFT_DECOUPLED=0 falls back to the fused first/last passes (A/B)
-inline bool decoupled_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("MWSHT_FFT_DECOUPLED");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 template <int LOGH, class K>
 static void launch_t(K kern, const FftArgs& a, int nsm, cudaStream_t st) {
   using C = Cfg<LOGH>;
@@ -1252,17 +1244,15 @@ static void launch_stage(int which, bool real, const FftArgs& a, int nsm, cudaSt
                 : launch_t<LOGH>(k_phi_fwd<false, LOGH>, a, nsm, st);
       break;
     case 1:
-      if constexpr (LOGH >= 11) {
-        if (decoupled_enabled()) {
-          real ? launch_t<LOGH>(k_theta_fwd2<true, LOGH>, a, nsm, st)
-               : sh ? launch_t<LOGH>(k_theta_fwd2<false, LOGH, true>, a, nsm, st)
-                    : launch_t<LOGH>(k_theta_fwd2<false, LOGH>, a, nsm, st);
-          break;
-        }
+      if constexpr (LOGH >= 11) {  // decoupled form (two rows per transform, TMEM parking)
+        real ? launch_t<LOGH>(k_theta_fwd2<true, LOGH>, a, nsm, st)
+             : sh ? launch_t<LOGH>(k_theta_fwd2<false, LOGH, true>, a, nsm, st)
+                  : launch_t<LOGH>(k_theta_fwd2<false, LOGH>, a, nsm, st);
+      } else {
+        real ? launch_t<LOGH>(k_theta_fwd<true, LOGH>, a, nsm, st)
+             : sh ? launch_t<LOGH>(k_theta_fwd<false, LOGH, true>, a, nsm, st)
+                  : launch_t<LOGH>(k_theta_fwd<false, LOGH>, a, nsm, st);
       }
-      real ? launch_t<LOGH>(k_theta_fwd<true, LOGH>, a, nsm, st)
-           : sh ? launch_t<LOGH>(k_theta_fwd<false, LOGH, true>, a, nsm, st)
-                : launch_t<LOGH>(k_theta_fwd<false, LOGH>, a, nsm, st);
       break;
     case 2:
       real ? launch_t<LOGH>(k_theta_inv<true, LOGH>, a, nsm, st)

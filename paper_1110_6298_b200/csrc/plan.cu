@@ -91,7 +91,7 @@ struct mwsht_plan {
   int M = 0, H = 0, logH = 0, nsm = 0, Q = 2;  // convolution length M = Q H
   double2* twM = nullptr;                      // Q = 4: quarter table of w_M
   double2 *tw = nullptr, *chirp = nullptr, *specf = nullptr, *speci = nullptr, *specw = nullptr,
-          *rho = nullptr, *scratch = nullptr, *cen = nullptr, *wnk = nullptr, *rho2 = nullptr;
+          *sep1 = nullptr, *sep2 = nullptr, *sep3 = nullptr, *scratch = nullptr, *cen = nullptr, *wnk = nullptr, *rho2 = nullptr;
   double2 *bufA = nullptr, *bufB = nullptr, *bufG = nullptr;
   long long strideA = 0, strideB = 0, strideG = 0;
   unsigned long long* red = nullptr;       // 2 device slots for the reality check (kept zero)
@@ -501,7 +501,7 @@ static int range_tiles(mwsht_plan* p, int m0, int m1, mwsht_plan::TileSet** out)
 // spectra (half-split DIF of the Bluestein kernels c, conj c and of the
 // weight-correlation kernel K'[d mod M] = 2 pi w(-d), |d| <= 2L-2,
 // quadrature.py:66-74, mw.py:237-238), and the forward theta glue
-// rho[k] = conj(c[k]) e^{-i f(k) pi/N} / (2 pi N M), f(k) = k (k < L), k - N,
+// (tau(f(k)) = e^{-i f(k) pi/N}, f(k) = k (k < L), k - N),
 // and for the paired forward theta rows (fft.cu): cen[k] = (-1)^k e^{i pi k/N},
 // wnk[k] = e^{2 pi i k/N}, rho2[k] = e^{-i f(k) pi/N} / (2 pi N M).
 static fft::FftArgs fft_args(mwsht_plan* p) {
@@ -517,7 +517,9 @@ static fft::FftArgs fft_args(mwsht_plan* p) {
   a.specf = p->specf;
   a.speci = p->speci;
   a.specw = p->specw;
-  a.rho = p->rho;
+  a.sep1 = p->sep1;
+  a.sep2 = p->sep2;
+  a.sep3 = p->sep3;
   a.cen = p->cen;
   a.wnk = p->wnk;
   a.rho2 = p->rho2;
@@ -550,7 +552,7 @@ static int build_fft_tables(mwsht_plan* p) {
   const ld PI = 3.141592653589793238462643383279502884L;
   // passes: quarter table of w_{2H} (= w_M at Q = 2); Q = 4 also w_M (global)
   const int M2 = 2 * p->H;
-  std::vector<double2> tw(M2 / 4 + 1), ch(N), rho(N), kf(M, make_double2(0, 0)), ki(kf), kw(kf);
+  std::vector<double2> tw(M2 / 4 + 1), ch(N), sep1(N), sep2(N), sep3(N), kf(M, make_double2(0, 0)), ki(kf), kw(kf);
   std::vector<double2> cen(N), wnk(N), rho2(N);
   auto quarter_table = [&](int Mt, std::vector<double2>& t) {
     t.assign(Mt / 4 + 1, make_double2(0, 0));
@@ -582,11 +584,19 @@ static int build_fft_tables(mwsht_plan* p) {
     const ld sc = 1.0L / (2.0L * PI * (ld)N * (ld)M);
     const ld tr = cosl(a) * sc, ti = sinl(a) * sc;
     // conj(c) * tau
-    rho[k] = make_double2((double)(cr[k] * tr + ci[k] * ti), (double)(cr[k] * ti - ci[k] * tr));
     rho2[k] = make_double2((double)tr, (double)ti);
     const ld b = PI * (ld)k / (ld)N, sg = (k & 1) ? -1.0L : 1.0L;
     cen[k] = make_double2((double)(sg * cosl(b)), (double)(sg * sinl(b)));
     wnk[k] = make_double2((double)cosl(2.0L * b), (double)sinl(2.0L * b));
+    // decoupled stage: the chirp and the 1/2 folded into the separation (common.cuh)
+    const ld hr = 0.5L * tr, hi = 0.5L * ti;
+    sep1[k] = make_double2((double)(cr[k] * hr + ci[k] * hi), (double)(cr[k] * hi - ci[k] * hr));
+    const int kn = (N - k) % N;
+    const ld wr = cosl(2.0L * b), wi = sinl(2.0L * b);                     // e^{2 pi i k/N}
+    const ld ur = wr * cr[kn] + wi * ci[kn], ui = wi * cr[kn] - wr * ci[kn];  // . conj(c[kn])
+    sep2[k] = make_double2((double)(hr * ur - hi * ui), (double)(hr * ui + hi * ur));
+    const ld er = sg * cosl(b), ei = sg * sinl(b);
+    sep3[k] = make_double2((double)(hr * er - hi * ei), (double)(hr * ei + hi * er));
   }
   for (int j = -(N - 1); j <= N - 1; j++) {
     const int n = j < 0 ? -j : j;
@@ -607,7 +617,8 @@ static int build_fft_tables(mwsht_plan* p) {
   }
   int rc;
   if ((rc = upload(p, &p->tw, tw)) || (rc = upload(p, &p->chirp, ch)) ||
-      (rc = upload(p, &p->rho, rho)) || (rc = upload(p, &p->cen, cen)) ||
+      (rc = upload(p, &p->sep1, sep1)) || (rc = upload(p, &p->sep2, sep2)) ||
+      (rc = upload(p, &p->sep3, sep3)) || (rc = upload(p, &p->cen, cen)) ||
       (rc = upload(p, &p->wnk, wnk)) || (rc = upload(p, &p->rho2, rho2)))
     return rc;
   double2 *dkf, *dki, *dkw;
