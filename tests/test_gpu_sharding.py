@@ -67,7 +67,7 @@ def _live_worker(rank, world, port, L, spin, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("L,spin,world", [(256, 2, 2), (300, 0, 3)])
+@pytest.mark.parametrize("L,spin,world", [(256, 2, 2), (300, 0, 3), (600, 1, 2)])  # 600: H = 2048
 def test_mcolumn_live_ranks_match_unsharded(L, spin, world):
     import socket
     import torch.multiprocessing as mp
