@@ -61,15 +61,15 @@ def test_forward_raw_signal_full_array(mw, O, L, spin):
     assert rel(got, ref) < 1e-12
 
 
-def test_forward_real_raw_signal_full_array_L1024(mw, O):
-    L = 1024
+@pytest.mark.parametrize("L", [1024, 601, 513])  # 601, 513: odd row counts, padded rows (H = 2048)
+def test_forward_real_raw_signal_full_array(mw, O, L):
     raw = random_signal(L, 0, 77).real.copy()
     got = mw.forward_real(mw.MwSignal(L, 0, raw)).values
     ref = O.forward_real(raw, L, "trapani", threads=THREADS)
     assert rel(got, ref) < 1e-12
 
 
-@pytest.mark.parametrize("L,spin", [(129, 0), (256, -2), (1024, 1)])
+@pytest.mark.parametrize("L,spin", [(129, 0), (256, -2), (1024, 1), (513, 0), (640, -1), (1025, 2)])
 def test_forward_stages_fft_branch(mw, O, L, spin):
     # L > 128: the oracle (like mw.py:232-251) correlates by FFT, not by matrix
     from paper_1110_6298_b200 import kernels
