@@ -459,14 +459,22 @@ def run_gpu(wl, steps, warmup, rank, ws, local, want_e2e=True, want_clocks=True,
         from paper_1110_6298_b200.pipeline import HostPipeline
         h_in = torch.from_numpy(host).pin_memory()
         h_out = torch.empty_like(h_in).pin_memory()
-        batched = nm > 1 and not real  # C4: the step's maps as one batch submission
+        # C4: the step's maps go through the pipeline as batch submissions of
+        # `sub` maps (two maps share each Wigner recursion in the cores, so
+        # pairs lose nothing against one batch of all maps, and the pipeline's
+        # fill and drain -- one H2D and one D2H without overlap -- shrink with
+        # the submission size)
+        batched = nm > 1 and not real
+        sub = int(os.environ.get("MWSHT_BENCH_SUB", "2"))
+        sub = sub if batched and nm % sub == 0 else nm
         pipe = HostPipeline(L, spin, kind="roundtrip", real=real, device=dev, depth=2,
-                            batch=nm if batched else None)
+                            batch=sub if batched else None)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
         def e2e_step():
             if batched:
-                pipe.submit(h_in, h_out)
+                for b in range(0, nm, sub):
+                    pipe.submit(h_in[b:b + sub], h_out[b:b + sub])
                 return
             for b in range(nm):
                 pipe.submit(h_in[b], h_out[b])
