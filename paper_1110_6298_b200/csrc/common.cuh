@@ -211,6 +211,7 @@ struct FftArgs {
   const long long* col_off;
   const int* col_stride;
   int spread;  // set by the launcher: rows dealt team-major (fft_impl.cuh first_row)
+  int pitch;   // inverse stages: row pitch of the ring plane between theta and phi synthesis (0: dense)
   int msp;                // multi-spin batch: map b's spin parity is bit b of spin_par
   unsigned long long spin_par;
   int Q;                  // convolution split: M = Q H (2, or 4 for 4096 < L <= 8192)

@@ -1027,7 +1027,7 @@ template <bool REAL, int LOGH, bool SH = false, int Q = 2>
 __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_inv(FftArgs a) {
   FFT_PROLOGUE
   const int L = a.L, N = a.N;
-  const int ocols = REAL ? L : N;
+  const int ocols = a.pitch ? a.pitch : (REAL ? L : N);
   const YStage<Q, LOGH> ys{X, scr + 3 * C::H};
   const double inv = 1.0 / (double)(Q * C::H);
   const int ntask = theta_tasks(a.m0, a.m1, REAL);
@@ -1065,17 +1065,33 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_inv(FftArgs a) {
       else
         return o[(long long)t * ocols + col[u]];
     };
+    // The task's two orders are neighbouring columns of the ring plane: with
+    // an even row pitch and the lower column even, both values of a ring go
+    // out as ONE aligned 32-byte store (a full sector) instead of two 16-byte
+    // halves -- these transposed stores, one 128-byte line per lane, are a
+    // fifth of the kernel (ncu: the store data held on the scoreboard).
+    const int clo = min(col[0], col[1]);
+    const bool wide = !SH && two && !(ocols & 1) && !(clo & 1) && col[0] + col[1] == 2 * clo + 1 &&
+                      (((unsigned long long)o & 31ull) == 0);
     for (int t = lt; t < L; t += C::TEAM) {
       const double2 z = ys(t);
-      double2 v1 = z;
+      double2 v1 = z, v2 = make_double2(0.0, 0.0);
       if (two) {
         const double2 zr = cscale(ys(N - 1 - t), e1);
         v1 = cscale(cadd(z, zr), 0.5);
         const double2 w = csub(z, zr);  // 2i y_2
-        oat(t, 1) = make_double2(0.5 * w.y, -0.5 * w.x);
+        v2 = make_double2(0.5 * w.y, -0.5 * w.x);
       }
       if (REAL && mr[0] == 0) v1.y = 0.0;  // irfft ignores Im of the DC bin
-      oat(t, 0) = v1;
+      if (wide) {
+        const double2 lo = col[0] < col[1] ? v1 : v2, hi = col[0] < col[1] ? v2 : v1;
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(o + (long long)t * ocols + clo),
+                     "d"(lo.x), "d"(lo.y), "d"(hi.x), "d"(hi.y)
+                     : "memory");
+      } else {
+        if (two) oat(t, 1) = v2;
+        oat(t, 0) = v1;
+      }
     }
     team_sync<C::TEAM>(team);
   }
@@ -1095,8 +1111,9 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_phi_inv(FftArgs a) {
     if (REAL) {
       const int tl = 2 * q, t = a.t0 + tl;
       const bool two = tl + 1 < a.nrows;
-      const double2* h = (const double2*)a.in + (long long)map * a.in_stride + (long long)t * L;
-      const double2* h2 = h + L;
+      const int pr = a.pitch ? a.pitch : L;
+      const double2* h = (const double2*)a.in + (long long)map * a.in_stride + (long long)t * pr;
+      const double2* h2 = h + pr;
       double* o = (double*)a.out + (long long)map * a.out_stride + (long long)tl * N;
       bluestein<LOGH, true, false, Q>(
           X, tws, scr, a, lt, team,
@@ -1115,7 +1132,8 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_phi_inv(FftArgs a) {
           });
     } else {
       const int tl = q, t = a.t0 + tl;
-      const double2* h = (const double2*)a.in + (long long)map * a.in_stride + (long long)t * N;
+      const double2* h = (const double2*)a.in + (long long)map * a.in_stride +
+                         (long long)t * (a.pitch ? a.pitch : N);
       double2* o = (double2*)a.out + (long long)map * a.out_stride + (long long)tl * N;
       auto hin = [&](int n) -> double2 {  // dense rows, or the shard receive layout
         if constexpr (SH)

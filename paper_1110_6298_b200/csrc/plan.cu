@@ -897,6 +897,8 @@ static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int
   f.in_stride = (long long)rows * N;
   f.out = p->bufA;
   f.out_stride = p->strideA;
+  // even row pitch of the ring plane: the paired theta rows store 32 bytes per ring
+  f.pitch = real ? (L + (L & 1)) : N + 1;
   fft_launch(2, real, f, p->nsm, st);
   LAUNCHED(p);
   // 3. phi synthesis (mw.py:437-438 / 558)
@@ -964,7 +966,7 @@ int mwsht_plan_create(int L, int device, int max_batch, mwsht_plan** out) {
     return fail(MWSHT_E_CUDA, "cudaSetDevice", cudaGetErrorString(e));
   }
   const long long L_ = L, N = p->N;
-  p->strideA = L_ * N;
+  p->strideA = L_ * (N + 1);  // (N, L) ring spectra (forward) / (L, N + 1) ring plane (inverse, even pitch)
   p->strideB = N * N;
   p->strideG = 2 * L_ * p->ldw;
   if ((rc = build_tables(p)) || (rc = build_tiles(p)) || (rc = build_fft_tables(p)) ||
