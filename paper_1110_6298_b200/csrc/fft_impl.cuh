@@ -479,10 +479,20 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_phi_fwd(FftArgs a) {
           });
       team_sync<C::TEAM>(team);
       const double h = 0.5 * sc;
+      // the two rings are neighbouring columns of AT: one aligned 32-byte store per bin
+      const bool wide = two && !(L & 1) && !(t & 1) && (((unsigned long long)at & 31ull) == 0);
       for (int k = lt; k < L; k += C::TEAM) {
         const double2 zk = ys(k), zn = ys(k ? N - k : 0);
-        at[(long long)k * L + t] = make_double2(h * (zk.x + zn.x), h * (zk.y - zn.y));
-        if (two) at[(long long)k * L + t + 1] = make_double2(h * (zk.y + zn.y), h * (zn.x - zk.x));
+        const double2 v1 = make_double2(h * (zk.x + zn.x), h * (zk.y - zn.y));
+        const double2 v2 = make_double2(h * (zk.y + zn.y), h * (zn.x - zk.x));
+        if (wide) {
+          asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(at + (long long)k * L + t),
+                       "d"(v1.x), "d"(v1.y), "d"(v2.x), "d"(v2.y)
+                       : "memory");
+        } else {
+          at[(long long)k * L + t] = v1;
+          if (two) at[(long long)k * L + t + 1] = v2;
+        }
       }
       team_sync<C::TEAM>(team);
     } else {
