@@ -201,8 +201,10 @@ int mwsht_plan_last_launches(const mwsht_plan *plan, int *own);
  *            writes its rings of the samples.
  * Local order row i enumerates +m0..+(m1-1), then -m0..-(m1-1) (m = 0 once).
  * The offset tables are device arrays built by the caller (shard.py); passing
- * NULL tables selects the dense single-GPU layouts (AT: N x L, row bin(m);
- * OUT: L x N, column bin(m)), which emulate_mcolumn uses. */
+ * NULL tables selects the dense single-GPU layouts, which emulate_mcolumn
+ * uses: OUT: L x N, column bin(m); AT: (N + 1) L values with the bins in pairs,
+ * bin k, ring t at ((k >> 1) L + t) 2 + (k & 1) (what both stages read and
+ * write with 32-byte accesses). */
 int mwsht_shard_forward_phi(mwsht_plan *plan, const void *samples_rows, int t0, int t1,
                             const long long *row_off, void *out, void *stream);
 int mwsht_shard_forward_rest(mwsht_plan *plan, const void *in, int m0, int m1,

@@ -358,6 +358,17 @@ __device__ __forceinline__ double2 rot_mi(double2 v, int q) {  // v (-i)^q
 
 __device__ __forceinline__ int fbin(int k, int N) { return k >= 0 ? k : k + N; }
 
+// Dense layout of the ring spectra AT between the forward phi and theta stages
+// (complex maps): bins go in pairs, at_idx(k, t) = ((k >> 1) L + t) 2 + (k & 1)
+// -- (N + 1) L entries.  The phi stage's transposed stores of neighbouring bins
+// (neighbouring lanes) then share a 32-byte sector, and the theta stage, whose
+// tasks are exactly these pairs (orders 2k, 2k+1; bins N-2k, N-2k-1), reads both
+// rows of a ring as one 32-byte load.  (16-byte stores one row apart cost the
+// phi stage 0.25 ms of 1.18 at L = 4096, timing probe.)
+__device__ __forceinline__ long long at_idx(int k, int t, int L) {
+  return ((long long)(k >> 1) * L + t) * 2 + (k & 1);
+}
+
 // Bluestein DFT_N of x (fx(n), n < N): forward (conj chirp, spec f) or inverse
 // (chirp, spec i).  Half 1 leaves z1 in scr; half 0 calls fin(k, y_k) with the
 // merged y[k] = z0[k] + w^-k z1[k] (unnormalised; DFT = chirp' . y / M).
@@ -503,7 +514,7 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_phi_fwd(FftArgs a) {
           if constexpr (SH)
             at[a.row_off[k] + tl] = v;  // shard send layout (per destination rank)
           else
-            at[(long long)k * L + t] = v;
+            at[at_idx(k, t, L)] = v;
         }
       };
       const double2* f = (const double2*)a.in + (long long)map * a.in_stride + (long long)tl * N;
@@ -578,14 +589,14 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_fwd(FftArgs a) {
       mr[u] = row_order(il[u], a.m0, a.m1, REAL);
       eps[u] = (((mr[u] + (REAL ? 0 : stage_spin(a, map))) & 1) ? -1.0 : 1.0);
       g[u] = (const double2*)a.in + (long long)map * a.in_stride +
-             (long long)(REAL ? mr[u] : fbin(mr[u], N)) * L;
+             (REAL ? (long long)mr[u] * L : at_idx(fbin(mr[u], N), 0, L));
     }
-    // ring t of row u: dense AT row, or the shard's receive layout
+    // ring t of row u: dense AT row (real) / bin pair (complex), or the shard's receive layout
     auto gin = [&](int u, int t) -> double2 {
       if constexpr (SH)
         return ((const double2*)a.in)[a.col_off[t] + (long long)il[u] * a.col_stride[t]];
       else
-        return g[u][t];
+        return g[u][REAL ? t : 2 * t];
     };
     // 1. Bluestein DFT_N of the periodic extension(s): X[k] = M Z[k]
     auto ext = [&](int u, int n) { return n < L ? gin(u, n) : cscale(gin(u, 2 * L - 2 - n), eps[u]); };
@@ -848,15 +859,19 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_fwd2(FftArgs a) {
       mr[u] = row_order(il[u], a.m0, a.m1, REAL);
       eps[u] = (((mr[u] + (REAL ? 0 : stage_spin(a, map))) & 1) ? -1.0 : 1.0);
       g[u] = (const double2*)a.in + (long long)map * a.in_stride +
-             (long long)(REAL ? mr[u] : fbin(mr[u], N)) * L;
+             (REAL ? (long long)mr[u] * L : at_idx(fbin(mr[u], N), 0, L));
     }
-    // ring t of row u: dense AT row, or the shard's receive layout
+    // ring t of row u: dense AT row (real) / bin pair (complex), or the shard's receive layout
     auto gin = [&](int u, int t) -> double2 {
       if constexpr (SH)
         return ((const double2*)a.in)[a.col_off[t] + (long long)il[u] * a.col_stride[t]];
       else
-        return g[u][t];
+        return g[u][REAL ? t : 2 * t];
     };
+    // complex dense layout: the task's two bins are one pair, both rows of a ring in 32 bytes
+    const bool pair32 = !REAL && !SH && two;
+    const double2* gpair = pair32 ? (g[0] < g[1] ? g[0] : g[1]) : nullptr;
+    const bool swapped = pair32 && g[1] < g[0];
     // A. Bluestein input xb[n] = (x_1 + i x_2)[n] conj(c[n]) of the extended rows:
     //    parked for half 0, times w^n into the row for half 1
 #pragma unroll
@@ -865,8 +880,17 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_fwd2(FftArgs a) {
 #pragma unroll
       for (int v = 0; v < B; v++) {
         const int n = min(O::pos(r0 + v, lt), N - 1), src = n < L ? n : 2 * L - 2 - n;
-        x1[v] = gin(0, src);
-        x2[v] = two ? gin(1, src) : make_double2(0.0, 0.0);
+        if (pair32) {
+          double2 lo, hi;
+          asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+                       : "=d"(lo.x), "=d"(lo.y), "=d"(hi.x), "=d"(hi.y)
+                       : "l"(gpair + 2 * src));
+          x1[v] = swapped ? hi : lo;
+          x2[v] = swapped ? lo : hi;
+        } else {
+          x1[v] = gin(0, src);
+          x2[v] = two ? gin(1, src) : make_double2(0.0, 0.0);
+        }
         ch[v] = a.chirp[n];
       }
 #pragma unroll

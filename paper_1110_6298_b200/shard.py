@@ -306,7 +306,7 @@ class MColumnSharding:
 def emulate_mcolumn(L, world, spin, flm, device=0):
     """Run the m-column-sharded inverse and forward of one map as `world`
     virtual ranks in one process, with the dense single-GPU layouts (NULL
-    offset tables: AT N x L, OUT L x N) shared by the virtual ranks instead of
+    offset tables: AT (N+1) x L in bin pairs, OUT L x N) shared by the virtual ranks instead of
     an exchange.  Validates the order/ring range logic of the shard stages."""
     from .mw import get_plan
     lib = _lib.load()
@@ -325,7 +325,7 @@ def emulate_mcolumn(L, world, spin, flm, device=0):
         _lib.check(lib.mwsht_shard_inverse_phi(plan.handle, OUT.data_ptr(), tb[r], tb[r + 1],
                                                None, None, samples[tb[r]].data_ptr(), st),
                    "shard_inverse_phi")
-    AT = torch.empty((N, L), dtype=torch.complex128, device=dev)
+    AT = torch.empty((N + 1, L), dtype=torch.complex128, device=dev)  # bins in pairs (mwsht.h)
     for r in range(world):
         rows = samples[tb[r]:tb[r + 1]].contiguous()
         _lib.check(lib.mwsht_shard_forward_phi(plan.handle, rows.data_ptr(), tb[r], tb[r + 1],
