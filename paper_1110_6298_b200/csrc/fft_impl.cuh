@@ -882,9 +882,10 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_fwd2(FftArgs a) {
         const int n = min(O::pos(r0 + v, lt), N - 1), src = n < L ? n : 2 * L - 2 - n;
         if (pair32) {
           double2 lo, hi;
-          asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
-                       : "=d"(lo.x), "=d"(lo.y), "=d"(hi.x), "=d"(hi.y)
-                       : "l"(gpair + 2 * src));
+          // (not volatile: the loads may move above the previous batch's stores like plain loads)
+          asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+              : "=d"(lo.x), "=d"(lo.y), "=d"(hi.x), "=d"(hi.y)
+              : "l"(gpair + 2 * src));
           x1[v] = swapped ? hi : lo;
           x2[v] = swapped ? lo : hi;
         } else {
