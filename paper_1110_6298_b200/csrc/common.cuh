@@ -131,6 +131,7 @@ struct InvArgs {
   const double2* gp;      // pre-scaled coefficients: gp[l*ldw+m] = c_l u_l(m) f_{l,m},
                           // gn = gp + L*ldw: c_l u_l(m) (-1)^l f_{l,-m}  (zero for m > l)
   double2* out;           // out_mode 0: theta-synthesis spectrum (N,N) [complex] / (L,N) [real]
+                          // out_mode 3: the same, bins m' >= 0 only (the mirrored half is not written)
                           // out_mode 1: raw T (L,N) [complex] / (L,L) [real]
   const double* wcol;     // paired tiles: [blk32(l, m)] = W_l(m) (the row weight at column indices)
   const int2* tiles;
@@ -212,6 +213,7 @@ struct FftArgs {
   const int* col_stride;
   int spread;  // set by the launcher: rows dealt team-major (fft_impl.cuh first_row)
   int pitch;   // inverse stages: row pitch of the ring plane between theta and phi synthesis (0: dense)
+  int half;    // inverse theta stage: the spectrum rows hold the m' >= 0 half only (core out_mode 3)
   int msp;                // multi-spin batch: map b's spin parity is bit b of spin_par
   unsigned long long spin_par;
   int Q;                  // convolution split: M = Q H (2, or 4 for 4096 < L <= 8192)

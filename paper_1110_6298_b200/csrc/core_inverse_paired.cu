@@ -404,6 +404,8 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
     const double2 tw = make_double2(cs, sn);    // e^{+i m' theta0}
     const double2 twc = make_double2(cs, -sn);  // e^{-i m' theta0}
     const int binp = x, binn = x ? N - x : 0;
+    // out_mode 3: the m' >= 0 half only (the theta stage rebuilds F[m, -m'] = +-F[m, m'] e^{-2 pi i m'/N})
+    const bool wmir = x && a.out_mode != 3;
     const double sx = (x & 1) ? -1.0 : 1.0;
     const double2 Tp = make_double2(pr, pi);
     if (a.out_mode == 1) {
@@ -420,19 +422,19 @@ __global__ void __launch_bounds__(kCoreThreadsWS, 1) k_inverse_core_paired(InvAr
       const double2 F = cmul(Tp, ipow(-m));
       double2* row = out + (long long)m * N;
       row[binp] = cmul(F, tw);
-      if (x) row[binn] = cscale(cmul(F, twc), (m & 1) ? -1.0 : 1.0);
+      if (wmir) row[binn] = cscale(cmul(F, twc), (m & 1) ? -1.0 : 1.0);
     } else {
       // F[m, m'] = (-1)^s i^{-(m+s)} T[m', m]; F[m, -m'] = (-1)^(m+s) F[m, m'] (mw.py:395-401)
       const double2 Fp = cscale(cmul(Tp, ipow(-(m + a.spin))), (double)sgs);
       double2* rowp = out + (long long)(L - 1 + m) * N;
       rowp[binp] = cmul(Fp, tw);
-      if (x) rowp[binn] = cscale(cmul(Fp, twc), ((m + a.spin) & 1) ? -1.0 : 1.0);
+      if (wmir) rowp[binn] = cscale(cmul(Fp, twc), ((m + a.spin) & 1) ? -1.0 : 1.0);
       if (m > 0) {
         const double2 Tn = make_double2(sx * nr, sx * ni);
         const double2 Fn = cscale(cmul(Tn, ipow(m - a.spin)), (double)sgs);
         double2* rown = out + (long long)(L - 1 - m) * N;
         rown[binp] = cmul(Fn, tw);
-        if (x) rown[binn] = cscale(cmul(Fn, twc), ((m + a.spin) & 1) ? -1.0 : 1.0);
+        if (wmir) rown[binn] = cscale(cmul(Fn, twc), ((m + a.spin) & 1) ? -1.0 : 1.0);
       }
     }
   };

@@ -98,12 +98,14 @@ __global__ void __launch_bounds__(kSmallThreads) k_inverse_small(InvArgs a) {
   sincospi((double)x / (double)N, &sn, &cs);
   const double2 tw = make_double2(cs, sn), twc = make_double2(cs, -sn);
   const int binp = x, binn = x ? N - x : 0;
+  // out_mode 3: bins m' >= 0 only (the theta stage rebuilds the mirrored half)
+  const bool wmir = x && a.out_mode != 3;
   if (REAL) {
     // fhalf[m, m'] = T[m', m] i^{-m}; mirror (-1)^m (mw.py:550-556)
     const double2 F = cmul(Tp, ipow(-m));
     double2* row = out + (long long)m * N;
     row[binp] = cmul(F, tw);
-    if (x) row[binn] = cscale(cmul(F, twc), (m & 1) ? -1.0 : 1.0);
+    if (wmir) row[binn] = cscale(cmul(F, twc), (m & 1) ? -1.0 : 1.0);
   } else {
     // F[m, m'] = (-1)^s i^{-(m+s)} T[m', m]; F[m, -m'] = (-1)^(m+s) F[m, m'] (mw.py:395-401)
     const int spin = a.spin;
@@ -111,13 +113,13 @@ __global__ void __launch_bounds__(kSmallThreads) k_inverse_small(InvArgs a) {
     const double2 Fp = cscale(cmul(Tp, ipow(-(m + spin))), sgs);
     double2* rowp = out + (long long)(L - 1 + m) * N;
     rowp[binp] = cmul(Fp, tw);
-    if (x) rowp[binn] = cscale(cmul(Fp, twc), ((m + spin) & 1) ? -1.0 : 1.0);
+    if (wmir) rowp[binn] = cscale(cmul(Fp, twc), ((m + spin) & 1) ? -1.0 : 1.0);
     if (m > 0) {
       const double sx = (x & 1) ? -1.0 : 1.0;
       const double2 Fn = cscale(cmul(make_double2(sx * an0, sx * an1), ipow(m - spin)), sgs);
       double2* rown = out + (long long)(L - 1 - m) * N;
       rown[binp] = cmul(Fn, tw);
-      if (x) rown[binn] = cscale(cmul(Fn, twc), ((m + spin) & 1) ? -1.0 : 1.0);
+      if (wmir) rown[binn] = cscale(cmul(Fn, twc), ((m + spin) & 1) ? -1.0 : 1.0);
     }
   }
 }

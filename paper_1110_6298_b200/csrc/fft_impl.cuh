@@ -1084,10 +1084,20 @@ __global__ void __launch_bounds__(Cfg<LOGH>::KT, 1) k_theta_inv(FftArgs a) {
     bluestein<LOGH, true, false, Q>(
         X, tws, scr, a, lt, team,
         [&](int n) {
-          const double2 s1 = sp[0][n];
-          if (!two) return s1;
-          const double2 s2 = sp[1][n];
-          return make_double2(s1.x - s2.y, s1.y + s2.x);  // S_1 + i S_2
+          // half rows (core out_mode 3): S[N - x] = eps_m S[x] e^{-2 pi i x/N}; the
+          // task's second order has the opposite sign, so S_1 + i S_2 mirrors to
+          // eps_1 (S_1 - i S_2)[x] conj(wnk[x])
+          const bool mirror = a.half && n >= L;
+          const int nn = mirror ? N - n : n;
+          const double2 s1 = sp[0][nn];
+          double2 v = s1;
+          if (two) {
+            const double2 s2 = sp[1][nn];
+            v = mirror ? make_double2(s1.x + s2.y, s1.y - s2.x)   // S_1 - i S_2
+                       : make_double2(s1.x - s2.y, s1.y + s2.x);  // S_1 + i S_2
+          }
+          if (mirror) v = cscale(cmulc(v, __ldg(&a.wnk[nn])), e1);
+          return v;
         },
         [&](int t, double2 y) {
           if (t < N) ys(t) = cscale(cmul(y, a.chirp[t]), inv);

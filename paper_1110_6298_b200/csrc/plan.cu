@@ -881,7 +881,7 @@ static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int
     }
   }
   a.out = p->bufB;
-  a.out_mode = 0;
+  a.out_mode = 3;  // m' >= 0 half of each spectrum row: the theta stage rebuilds the mirror
   a.out_stride = (long long)rows * N;
   core_inverse(p, a, inv_ntiles(p, a), nm, real, st);
   LAUNCHED(p);
@@ -894,6 +894,7 @@ static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int
   f.nmaps = nm;
   f.nrows = rows;
   f.in = p->bufB;
+  f.half = 1;
   f.in_stride = (long long)rows * N;
   f.out = p->bufA;
   f.out_stride = p->strideA;
@@ -1301,7 +1302,7 @@ int mwsht_shard_inverse_front(mwsht_plan* p, const void* flm, int m0, int m1, in
   a.paired = 0;  // order-restricted tiles: the transpose would leave the shard's orders
   a.tiles = ts->inv;
   a.out = p->bufB;
-  a.out_mode = 0;
+  a.out_mode = 3;
   a.out_stride = (long long)N * N;
   if (ts->ninv) {
     launch_inverse_core(a, ts->ninv, 1, false, st);
@@ -1313,6 +1314,7 @@ int mwsht_shard_inverse_front(mwsht_plan* p, const void* flm, int m0, int m1, in
   f.m1 = m1;
   f.nrows = 2 * (m1 - m0) - (m0 == 0 ? 1 : 0);
   f.in = p->bufB;
+  f.half = 1;
   f.in_stride = 0;
   f.out = out;
   f.out_stride = 0;
