@@ -18,6 +18,9 @@
 //   k_phi_fwd    mw.py:149-158 / :489   samples row t -> AT[k][t] = 2pi/N DFT_N (transposed)
 //   k_theta_fwd  mw.py:161-285           AT row -> extension -> DFT_N -> twist -> weight
 //                                        correlation -> m' fold -> core staging (gfT)
+//   k_theta_fwd2                         the same stage for H >= 2048, decoupled: shared-memory-only
+//                                        half-convolutions + element-wise global loops, waiting
+//                                        rows parked in tensor memory (see conv_smem)
 //   k_theta_inv  mw.py:441-446           spectrum row m -> IDFT_N -> Out[t][bin(m)], t < L
 //   k_phi_inv    mw.py:437-438 / :558    Out row t -> IDFT_N -> samples row t
 //   k_spectrum   plan time: S_0, S_1 of a length-M kernel
