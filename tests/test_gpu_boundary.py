@@ -20,12 +20,13 @@ def mw():
     return m
 
 
-def test_two_threads_two_streams_share_one_plan(mw):
+@pytest.mark.parametrize("L", [512, 640])  # 640: H = 2048, the tensor-memory theta stage
+def test_two_threads_two_streams_share_one_plan(mw, L):
     # both threads hit the same cached (L, device) plan, each on its own torch
     # stream; the library's event hand-off keeps their scratch use ordered
     import torch
     from oracle import mw_oracle as O
-    L, spin, reps = 512, 2, 6
+    spin, reps = 2, 6
     vals = [torch.from_numpy(O.gaussian_coeffs(L, spin, 60 + k)).cuda() for k in range(2)]
     expect = []
     for v in vals:
