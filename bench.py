@@ -95,6 +95,22 @@ def stage_bytes(L, real):
     return b / 2 if real else b
 
 
+def inv_stage_bytes(L, real):
+    """§8(d) algorithmic HBM bytes of the inverse stages around the core
+    (mirror fill, theta synthesis, phi synthesis; no convolution there)."""
+    N = 2 * L - 1
+    b = 16 * ((N * L + N * N) + (N * N + L * N) + 2 * L * N)
+    return b / 2 if real else b
+
+
+def inv_stage_flops(L, real):
+    """5 n log2 n flops of the inverse FFT stages per map: the theta DFT_N of
+    each order row and the phi DFT_N of each ring."""
+    N = 2 * L - 1
+    f = (N + L) * 5.0 * N * math.log2(N)
+    return f / 2 if real else f
+
+
 def stage_flops(L, real):
     """Algorithmic FP64 flops of the forward FFT stages per map, counting an
     n-point complex FFT as 5 n log2 n: the phi DFT_N of L rings, then per
@@ -399,9 +415,9 @@ def run_gpu(wl, steps, warmup, rank, ws, local, want_e2e=True, want_clocks=True,
     def core_times():
         c, s = _lib.ctypes.c_float(), _lib.ctypes.c_float()
         lib.mwsht_plan_last_timing(plan.handle, 1, _lib.ctypes.byref(c), _lib.ctypes.byref(s))
-        inv_core = c.value
+        inv_core, inv_stage = c.value, s.value
         lib.mwsht_plan_last_timing(plan.handle, 0, _lib.ctypes.byref(c), _lib.ctypes.byref(s))
-        return inv_core, c.value, s.value
+        return inv_core, c.value, s.value, inv_stage
 
     for _ in range(warmup):
         step()
@@ -431,16 +447,17 @@ def run_gpu(wl, steps, warmup, rank, ws, local, want_e2e=True, want_clocks=True,
     clk = clocks.stop() if clocks else None
     # per-kernel attribution pass (not part of `value`): events around the cores
     _lib.check(lib.mwsht_plan_set_timing(plan.handle, 1), "set_timing")
-    inv_core = fwd_core = fwd_stage = 0.0
+    inv_core = fwd_core = fwd_stage = inv_stage = 0.0
     for k in range(steps):
         if flush is not None:
             flush.zero_()
         step()
         torch.cuda.synchronize()
-        a, b, c = core_times()
+        a, b, c, d = core_times()
         inv_core += a
         fwd_core += b
         fwd_stage += c
+        inv_stage += d
     _lib.check(lib.mwsht_plan_set_timing(plan.handle, 0), "set_timing")
     total_ms = max_over_ranks(float(np.sum(step_ms)), ws)
     # the attribution pass times the last map of each step's batch/loop only for
@@ -448,8 +465,8 @@ def run_gpu(wl, steps, warmup, rank, ws, local, want_e2e=True, want_clocks=True,
     per = nm if real else 1
     out = dict(total_ms=total_ms, steps=steps, maps_per_rank=nm, launches=launches // steps,
                inv_core_ms=inv_core / steps * per, fwd_core_ms=fwd_core / steps * per,
-               fwd_stages_ms=fwd_stage / steps * per, roundtrip_err=err, clocks=clk,
-               plan_bytes=plan.device_bytes())
+               fwd_stages_ms=fwd_stage / steps * per, inv_stages_ms=inv_stage / steps * per,
+               roundtrip_err=err, clocks=clk, plan_bytes=plan.device_bytes())
 
     if want_e2e:
         # Public API with pinned host buffers: every step copies its coefficients
@@ -625,6 +642,9 @@ def summarize(key, wl, r, ws, peak_tf, steps, warmup):
               if r["fwd_stages_ms"] > 0 else None)
     st_tf = (stage_flops(L, real) * nm / (r["fwd_stages_ms"] / 1e3) / 1e12
              if r["fwd_stages_ms"] > 0 else None)
+    ims = r.get("inv_stages_ms", 0.0)
+    ist_gbs = inv_stage_bytes(L, real) * nm / (ims / 1e3) / 1e9 if ims > 0 else None
+    ist_tf = inv_stage_flops(L, real) * nm / (ims / 1e3) / 1e12 if ims > 0 else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": steps,
         "warmup": warmup, "ms_per_step": r["total_ms"] / steps, "higher_is_better": True,
@@ -646,7 +666,13 @@ def summarize(key, wl, r, ws, peak_tf, steps, warmup):
                              "bytes": "SURVEY §8(d) stage bytes, core term excluded",
                              "fp64_tflops": st_tf,
                              "fp64_frac": (st_tf / peak_tf) if (st_tf and peak_tf) else None,
-                             "flops": "5 n log2 n per FFT (bench.stage_flops)"}}},
+                             "flops": "5 n log2 n per FFT (bench.stage_flops)"},
+                         "inverse_fft_stages": {
+                             "ms": ims, "gbs": ist_gbs, "hbm_peak_gbs": hbm,
+                             "frac": (ist_gbs / hbm) if (ist_gbs and hbm) else None,
+                             "bytes": "SURVEY §8(d): fill + theta synthesis + phi synthesis",
+                             "fp64_tflops": ist_tf,
+                             "fp64_frac": (ist_tf / peak_tf) if (ist_tf and peak_tf) else None}}},
         "gpu_launches": r["launches"] * steps,
         "roundtrip_max_abs_err": r["roundtrip_err"],
         "clocks": r["clocks"],
@@ -671,6 +697,7 @@ def compact(line):
            "fwd_core_ms": round(rf["kernels"]["forward_core"]["ms"], 4),
            "inv_core_ms": round(rf["kernels"]["inverse_core"]["ms"], 4),
            "fwd_stages_ms": round(rf["kernels"]["forward_fft_stages"]["ms"], 4),
+           "inv_stages_ms": round(rf["kernels"]["inverse_fft_stages"]["ms"], 4),
            "roundtrip_err": line["roundtrip_max_abs_err"], "launches": line["gpu_launches"]}
     if "cpu_baseline" in line:
         out["cpu_pairs_s"] = line["cpu_baseline"]["value"]

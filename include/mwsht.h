@@ -251,8 +251,9 @@ int mwsht_plan_set_paired(mwsht_plan *plan, int mode);
  * enabled, each transform records CUDA events on its stream around the FFT
  * stages and around the core kernel; last_timing synchronises on them. */
 int mwsht_plan_set_timing(mwsht_plan *plan, int on);
-/* inverse = 0: last forward call (stages_ms = FFT stages before the core);
- * inverse = 1: last inverse call (stages_ms = 0, the core runs first). */
+/* inverse = 0: last forward call (stages_ms = the FFT stages, which run before
+ * the core); inverse = 1: last inverse call (stages_ms = the theta and phi
+ * synthesis stages, which run after it). */
 int mwsht_plan_last_timing(mwsht_plan *plan, int inverse, float *core_ms, float *stages_ms);
 
 /* DFMA throughput probe (FP64 roofline denominator): TFLOP/s reached by a

@@ -99,7 +99,7 @@ struct mwsht_plan {
   unsigned long long* red_host_dev = nullptr;
   int own_launches = 0;
   bool timing = false;
-  cudaEvent_t ev[2][3] = {};  // [forward|inverse][start, core start, core end]
+  cudaEvent_t ev[2][4] = {};  // [forward|inverse][start, core start, core end, end]
   double* colc = nullptr;  // [blk32(l, m)] = C_l(m)
   std::vector<long double> hl_A, hl_V, hl_Bt, hl_lam, hl_kap;  // host tables for the spin builds
   std::mutex mu;
@@ -910,6 +910,7 @@ static int do_inverse(mwsht_plan* p, int nm, const void* flm, void* samples, int
   f.out_stride = (long long)L * N;
   fft_launch(3, real, f, p->nsm, st);
   LAUNCHED(p);
+  if (p->timing) CU(cudaEventRecord(p->ev[1][3], st));
   return MWSHT_OK;
 }
 
@@ -1419,10 +1420,14 @@ int mwsht_plan_last_timing(mwsht_plan* p, int inverse, float* core_ms, float* st
   if ((rc = check_plan(p, dg))) return rc;
   if (!p->timing) return fail(MWSHT_E_VALUE, "last_timing", "timing not enabled");
   cudaEvent_t* e = p->ev[inverse ? 1 : 0];
-  CU(cudaEventSynchronize(e[2]));
+  CU(cudaEventSynchronize(e[inverse ? 3 : 2]));
   float c = 0.f, s0 = 0.f;
   CU(cudaEventElapsedTime(&c, e[1], e[2]));
-  CU(cudaEventElapsedTime(&s0, e[0], e[1]));
+  // forward: the FFT stages run before the core; inverse: after it
+  if (inverse)
+    CU(cudaEventElapsedTime(&s0, e[2], e[3]));
+  else
+    CU(cudaEventElapsedTime(&s0, e[0], e[1]));
   if (core_ms) *core_ms = c;
   if (stages_ms) *stages_ms = s0;
   return MWSHT_OK;
